@@ -1,0 +1,189 @@
+/*
+ * teal_b200.h — C ABI of the B200-native TEAL decode hot path.
+ *
+ * Every entry point takes caller-owned DEVICE pointers, plain sizes and a
+ * cudaStream_t, returns an int status (TEAL_OK = 0) and never allocates,
+ * frees or synchronises.  The last error message of the calling thread is
+ * available from teal_last_error().  No C++ exception crosses this boundary.
+ * All launches are stream-ordered and CUDA-graph capturable.
+ *
+ * Reference interfaces replaced (paths relative to the reference tree):
+ *   teal_threshold         <- sparsifier.sparsify / realized_sparsity
+ *                             (pkg/src/actsparse/sparsifier.py:120-133)
+ *   teal_threshold_batched <- sparsifier.sparsify_batched (sparsifier.py:136-155)
+ *   teal_sparse_gemv       <- kernel.sparse_gemv -> _skip_gemv numba FFI
+ *                             (pkg/src/actsparse/kernel.py:30-65, call site :62)
+ *   teal_dense_gemv        <- tensor.matmul_dense -> _gemv_{row,col}major
+ *                             (pkg/src/actsparse/tensor.py:107-140)
+ *   teal_fused_gemv        <- the seven `gated(name, a) @ W.T` sites of
+ *                             model._forward (pkg/src/actsparse/model.py:166-198)
+ *                             with RMSNorm prologue (model.py:126-128),
+ *                             SiLU(gate)*up epilogue (model.py:131-132,191-193)
+ *                             and residual adds (model.py:184,198)
+ *   teal_hist_record       <- ActivationHistogram.record (sparsifier.py:68-83)
+ *   teal_hist_threshold    <- ActivationHistogram.threshold (sparsifier.py:94-117)
+ *   teal_decode_attention  <- model._causal_attention, row t (model.py:135-150)
+ */
+#ifndef TEAL_B200_H
+#define TEAL_B200_H
+
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TEAL_ABI_VERSION 1
+
+/* status codes */
+#define TEAL_OK 0
+#define TEAL_EINVAL 1   /* invalid argument (message via teal_last_error) */
+#define TEAL_ECUDA 2    /* CUDA launch / runtime error */
+
+/* element types */
+#define TEAL_F32 0
+#define TEAL_BF16 1
+#define TEAL_I8 2       /* int8 rows, per-output-column fp32 scale */
+
+/* fused-GEMV prologues: how the input h is formed from x */
+#define TEAL_PRO_PLAIN 0     /* h_i = x_i */
+#define TEAL_PRO_RMSNORM 1   /* h_i = x_i / sqrt(sum(ss_part)/m + eps) * norm_scale_i */
+
+/* fused-GEMV epilogues */
+#define TEAL_EPI_STORE 0     /* seg.y[j] = acc_j                          */
+#define TEAL_EPI_RESID 1     /* resid[j] += acc_j ; ss_out[tile] = sum x^2 */
+#define TEAL_EPI_SILU 2      /* inter[j] = silu(acc_gate_j) * acc_up_j    */
+#define TEAL_EPI_QKV 3       /* q -> rope -> q_out ; k -> rope -> k cache ; v -> v cache */
+
+const char* teal_last_error(void);
+int teal_abi_version(void);
+int teal_device_sm_count(int device);
+
+/* ---- thresholding ------------------------------------------------------ */
+
+/* keep_i = !(|x_i| <= t32)  (closed prune boundary, NaN kept).
+ * keep_bits (nullable): bit i%32 of word i/32 set iff kept; [ceil(m/32)] words.
+ * x_sparse  (nullable): x with pruned entries replaced by +0.0, same dtype as x.
+ * pruned    (nullable): atomically incremented by the number of pruned entries. */
+int teal_threshold(const void* x, int x_dtype, int64_t m, float t32,
+                   uint32_t* keep_bits, void* x_sparse,
+                   unsigned long long* pruned, cudaStream_t stream);
+
+/* Shared column mask over a [B, m] fp32 batch: column i pruned iff
+ * (sum_b |X[b,i]| in ascending b, fp32) / B <= t32.  mask[i] = 1 if pruned.
+ * xs_sparse (nullable) receives the batch with pruned columns zeroed. */
+int teal_threshold_batched(const float* xs, int64_t B, int64_t m, float t32,
+                           uint8_t* mask, float* xs_sparse, cudaStream_t stream);
+
+/* ---- GEMV over input-major (transposed) weights ------------------------ */
+
+/* One projection inside a fused launch.  Element (input i, output j) of the
+ * segment lives at w[i*ldw + j] (the reference's COL_MAJOR layout of the
+ * logical [n_out, m_in] matrix, tensor.py:47-48). */
+typedef struct teal_seg {
+    const void* w;               /* weights, w_dtype elements                   */
+    int64_t ldw;                 /* row stride in elements (>= n)              */
+    int64_t n;                   /* output columns                              */
+    float t32;                   /* keep iff !(|h_i| <= t32); -INFINITY = dense */
+    float* y;                    /* EPI_STORE output [n] fp32                   */
+    const float* col_scale;      /* TEAL_I8 only: per-output-column scale [n]   */
+    uint32_t* dbg_bits;          /* nullable: keep bitmask of h [ceil(m/32)]    */
+    unsigned long long* kept;    /* nullable: += kept input channels            */
+} teal_seg;
+
+typedef struct teal_gemv_args {
+    int w_dtype;                 /* TEAL_F32 / TEAL_BF16 / TEAL_I8              */
+    int x_dtype;                 /* TEAL_F32 / TEAL_BF16 (PRO_PLAIN only)       */
+    const void* x;               /* input vector [m]                            */
+    int64_t m;                   /* input channels                              */
+    int nseg;                    /* 1..3                                        */
+    teal_seg seg[3];
+    /* prologue */
+    int prologue;
+    const float* norm_scale;     /* RMSNorm gain [m]                            */
+    const float* ss_part;        /* fp32 partial sums of x^2, summed in order   */
+    int ss_count;
+    float eps;
+    float* dbg_h;                /* nullable: h [m] fp32 (written once)         */
+    /* epilogue */
+    int epilogue;
+    float* resid;                /* EPI_RESID: residual stream [n], updated     */
+    float* ss_out;               /* EPI_RESID: [tiles] partial sum of squares   */
+    float* inter;                /* EPI_SILU: [n]                               */
+    float* q_out;                /* EPI_QKV: rotated q [n_q]                    */
+    void* k_cache;               /* EPI_QKV: [kv_heads][max_seq][head_dim]      */
+    void* v_cache;
+    int kv_dtype;                /* TEAL_F32 / TEAL_BF16                        */
+    int64_t max_seq;
+    const int* pos;              /* device scalar: position being written       */
+    int head_dim;
+    const float* rope_cos;       /* nullable (no RoPE): [max_seq][head_dim/2]   */
+    const float* rope_sin;
+    /* split-K and workspace (caller-owned) */
+    int ksplit;                  /* number of K chunks                          */
+    int kchunk;                  /* channels per chunk, multiple of 32          */
+    float* ws;                   /* [ksplit][sum n] fp32 partials               */
+    uint32_t* tickets;           /* [tiles], zero before first use; self-reset  */
+    int tile_override;           /* 0 = auto                                    */
+} teal_gemv_args;
+
+/* Launch plan: fills ksplit/kchunk and returns the column tile width used for
+ * this (w_dtype, n alignment).  ws needs ksplit*ncols_total floats, tickets
+ * needs teal_gemv_tiles() words. */
+int teal_gemv_plan(int64_t m, int64_t ncols_total, int w_dtype, int nseg,
+                   int* ksplit, int* kchunk);
+int teal_gemv_tile_width(const teal_gemv_args* a);
+int teal_gemv_tiles(const teal_gemv_args* a);
+int teal_fused_gemv(const teal_gemv_args* a, cudaStream_t stream);
+
+/* Convenience single-projection forms (kernel.py:30-65 / tensor.py:137-140). */
+int teal_sparse_gemv(const void* w, int w_dtype, int64_t m, int64_t n, int64_t ldw,
+                     const void* x, int x_dtype, float t32, float* y,
+                     const float* col_scale,
+                     float* ws, uint32_t* tickets, int ksplit, int kchunk,
+                     unsigned long long* kept, cudaStream_t stream);
+int teal_dense_gemv(const void* w, int w_dtype, int64_t m, int64_t n, int64_t ldw,
+                    const void* x, int x_dtype, float* y, const float* col_scale,
+                    float* ws, uint32_t* tickets, int ksplit, int kchunk,
+                    cudaStream_t stream);
+
+/* ---- calibration ------------------------------------------------------- */
+
+/* counts[b] += #{i : floor(|x_i|/hi*bins) clipped to bins-1 == b, |x_i| <= hi}
+ * overflow  += #{i : |x_i| > hi};  nan_flag set to 1 if any NaN.
+ * Binning in fp64 exactly as numpy (sparsifier.py:75-80). */
+int teal_hist_record(const void* x, int x_dtype, int64_t count, double hi, int bins,
+                     unsigned long long* counts, unsigned long long* overflow,
+                     unsigned int* nan_flag, cudaStream_t stream);
+
+/* Thresholds for np levels p[] from one histogram (sparsifier.py:94-117);
+ * total = sum(counts) + overflow.  One CTA, fp64, results bit-identical to
+ * the reference's numpy arithmetic. */
+int teal_hist_threshold(const unsigned long long* counts, int bins,
+                        const unsigned long long* overflow, double hi,
+                        const double* p, int np_, double* t_out, cudaStream_t stream);
+
+/* ---- decode-step helpers ----------------------------------------------- */
+
+/* ctx[h*hd + d] = softmax_u(q_h . k_u / sqrt(hd)) v_u over positions u < *len,
+ * GQA: q head h reads kv head h / (H / KVH). */
+int teal_decode_attention(const float* q, const void* k_cache, const void* v_cache,
+                          int kv_dtype, int H, int KVH, int hd, int64_t max_seq,
+                          const int* len, int max_len, float* ctx,
+                          float* ws, uint32_t* tickets, int nsplit,
+                          cudaStream_t stream);
+
+/* x = float(src) (src row = emb + (*token)*d when token != NULL, else src);
+ * ss_out[t] = sum of x^2 over columns [t*tile, (t+1)*tile). */
+int teal_load_residual(const void* src, int src_dtype, const int* token, int64_t d,
+                       float* x, float* ss_out, int tile, cudaStream_t stream);
+
+/* out_token = argmax(logits) (lowest index on ties, NaN ignored). */
+int teal_argmax(const float* logits, int64_t n, int* out_token,
+                float* ws, uint32_t* tickets, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TEAL_B200_H */

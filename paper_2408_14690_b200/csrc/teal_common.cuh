@@ -1,0 +1,101 @@
+// Shared device helpers for the TEAL sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <math.h>
+#include "teal_b200.h"
+
+namespace teal {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+// ---- error reporting (thread-local message, no exceptions across the ABI) --
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+
+#define TEAL_REQUIRE(cond, ...)            \
+    do {                                   \
+        if (!(cond)) {                     \
+            ::teal::set_error(__VA_ARGS__); \
+            return TEAL_EINVAL;            \
+        }                                  \
+    } while (0)
+
+// ---- element conversion ----------------------------------------------------
+__device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_float(((uint32_t)h) << 16); }
+__device__ __forceinline__ uint16_t f32_to_bf16_rn(float f) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+template <typename T> __device__ __forceinline__ float to_f32(T v);
+template <> __device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f32<uint16_t>(uint16_t v) { return bf16_to_f32(v); }
+template <> __device__ __forceinline__ float to_f32<int8_t>(int8_t v) { return (float)v; }
+
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ uint16_t from_f32<uint16_t>(float v) { return f32_to_bf16_rn(v); }
+
+// ---- streaming loads ---------------------------------------------------------
+// 256-bit non-coherent load, no L1 allocation, L2 evict-first (weights are read
+// exactly once per decode step; keep L2 for activations, partials and KV).
+struct alignas(32) U8 { uint32_t v[8]; };
+
+__device__ __forceinline__ U8 ldg256_stream(const void* p) {
+    U8 r;
+    asm volatile(
+        "ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]),
+          "=r"(r.v[4]), "=r"(r.v[5]), "=r"(r.v[6]), "=r"(r.v[7])
+        : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint4 ldg128_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// L2-coherent scalar load used when reading other CTAs' split-K partials.
+__device__ __forceinline__ float ldcg_f32(const float* p) { return __ldcg(p); }
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Deterministic block-wide sum (fixed tree: warp xor-reduce, then warp 0 over
+// the per-warp values in ascending warp order).  All threads get the result.
+__device__ __forceinline__ float block_sum(float v, float* s_scratch /*[kWarps+1]*/) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) s_scratch[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) t += s_scratch[w];
+        s_scratch[kWarps] = t;
+    }
+    __syncthreads();
+    float r = s_scratch[kWarps];
+    __syncthreads();
+    return r;
+}
+
+}  // namespace teal
