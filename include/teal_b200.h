@@ -120,33 +120,35 @@ typedef struct teal_gemv_args {
     int head_dim;
     const float* rope_cos;       /* nullable (no RoPE): [max_seq][head_dim/2]   */
     const float* rope_sin;
-    /* split-K and workspace (caller-owned) */
-    int ksplit;                  /* number of K chunks                          */
-    int kchunk;                  /* channels per chunk, multiple of 32          */
-    float* ws;                   /* [ksplit][sum n] fp32 partials               */
-    uint32_t* tickets;           /* [tiles], zero before first use; self-reset  */
-    int tile_override;           /* 0 = auto                                    */
+    /* persistent split-K grid and workspace (caller-owned) */
+    int ctas;                    /* CTAs (0 = auto: CTAS_PER_SM x #SMs)         */
+    float* ws;                   /* split-K partials, teal_gemv_workspace() floats */
+    uint32_t* tickets;           /* one per column tile, zero before first use;
+                                    self-resetting (graph-replay safe)          */
 } teal_gemv_args;
 
-/* Launch plan: fills ksplit/kchunk and returns the column tile width used for
- * this (w_dtype, n alignment).  ws needs ksplit*ncols_total floats, tickets
- * needs teal_gemv_tiles() words. */
-int teal_gemv_plan(int64_t m, int64_t ncols_total, int w_dtype, int nseg,
-                   int* ksplit, int* kchunk);
+/* Work decomposition: the (column tile, 32-channel group) space of all
+ * segments is flattened tile-major and split into `ctas` equal contiguous
+ * ranges, one per CTA of a single persistent wave; a column tile shared by
+ * several CTAs is reduced by its last-arriving CTA in ascending-CTA order.
+ * teal_gemv_workspace() resolves ctas=0 and reports the ws/ticket sizes. */
+int teal_gemv_workspace(const teal_gemv_args* a, int* ctas, int64_t* ws_floats,
+                        int64_t* tickets);
 int teal_gemv_tile_width(const teal_gemv_args* a);
-int teal_gemv_tiles(const teal_gemv_args* a);
+/* Debug: copy n per-CTA phase timestamps of the last launch run with
+ * TEAL_TIMELINE=1 in the environment (synchronous; not for the hot path). */
+int teal_debug_timeline(unsigned long long* host_dst, int n);
 int teal_fused_gemv(const teal_gemv_args* a, cudaStream_t stream);
 
 /* Convenience single-projection forms (kernel.py:30-65 / tensor.py:137-140). */
 int teal_sparse_gemv(const void* w, int w_dtype, int64_t m, int64_t n, int64_t ldw,
                      const void* x, int x_dtype, float t32, float* y,
                      const float* col_scale,
-                     float* ws, uint32_t* tickets, int ksplit, int kchunk,
+                     float* ws, uint32_t* tickets, int ctas,
                      unsigned long long* kept, cudaStream_t stream);
 int teal_dense_gemv(const void* w, int w_dtype, int64_t m, int64_t n, int64_t ldw,
                     const void* x, int x_dtype, float* y, const float* col_scale,
-                    float* ws, uint32_t* tickets, int ksplit, int kchunk,
-                    cudaStream_t stream);
+                    float* ws, uint32_t* tickets, int ctas, cudaStream_t stream);
 
 /* ---- calibration ------------------------------------------------------- */
 
@@ -175,9 +177,13 @@ int teal_decode_attention(const float* q, const void* k_cache, const void* v_cac
                           cudaStream_t stream);
 
 /* x = float(src) (src row = emb + (*token)*d when token != NULL, else src);
- * ss_out[t] = sum of x^2 over columns [t*tile, (t+1)*tile). */
+ * ss_out[t] = sum of x^2 over columns [t*tile, (t+1)*tile).
+ * step_state (nullable) = {pos, len}: starts a decode step — pos = len,
+ * len = len + 1 (pos is the KV position this step writes, len the attended
+ * length), so a captured graph of one step replays token after token. */
 int teal_load_residual(const void* src, int src_dtype, const int* token, int64_t d,
-                       float* x, float* ss_out, int tile, cudaStream_t stream);
+                       float* x, float* ss_out, int tile, int* step_state,
+                       cudaStream_t stream);
 
 /* out_token = argmax(logits) (lowest index on ties, NaN ignored). */
 int teal_argmax(const float* logits, int64_t n, int* out_token,

@@ -13,6 +13,7 @@ constexpr int kWarps = kThreads / 32;
 
 // ---- error reporting (thread-local message, no exceptions across the ABI) --
 void set_error(const char* fmt, ...);
+int pdl_enabled();  // TEAL_PDL=0 disables programmatic dependent launch
 int check_launch(const char* what);
 
 #define TEAL_REQUIRE(cond, ...)            \
@@ -79,23 +80,65 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
-// Deterministic block-wide sum (fixed tree: warp xor-reduce, then warp 0 over
-// the per-warp values in ascending warp order).  All threads get the result.
-__device__ __forceinline__ float block_sum(float v, float* s_scratch /*[kWarps+1]*/) {
+// Deterministic block-wide sum (fixed tree: warp xor-reduce, then thread 0
+// over the per-warp values in ascending warp order).  All threads get the
+// result.  s_scratch holds blockDim.x/32 + 1 floats (<= 33).
+__device__ __forceinline__ float block_sum(float v, float* s_scratch) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
     v = warp_sum(v);
     if (lane == 0) s_scratch[warp] = v;
     __syncthreads();
     if (threadIdx.x == 0) {
         float t = 0.f;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) t += s_scratch[w];
-        s_scratch[kWarps] = t;
+        for (int w = 0; w < nw; ++w) t += s_scratch[w];
+        s_scratch[nw] = t;
     }
     __syncthreads();
-    float r = s_scratch[kWarps];
+    float r = s_scratch[nw];
     __syncthreads();
     return r;
+}
+
+// ---- mbarrier + bulk async copy (TMA engine, no tensor map) -------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// global -> shared bulk copy completing `bytes` of transaction count on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
 }
 
 }  // namespace teal

@@ -130,8 +130,13 @@ __global__ void __launch_bounds__(kThreads) attention_kernel(const float* __rest
 template <typename ST>
 __global__ void __launch_bounds__(kThreads) load_residual_kernel(const ST* __restrict__ src, const int* __restrict__ token,
                                                                  int64_t d, float* __restrict__ x,
-                                                                 float* __restrict__ ss_out, int tile) {
+                                                                 float* __restrict__ ss_out, int tile, int* step_state) {
     __shared__ float s_scr[kWarps + 1];
+    if (step_state && blockIdx.x == 0 && threadIdx.x == 0) {  // {pos, len}: this step writes position len_prev
+        const int len = step_state[1];
+        step_state[0] = len;
+        step_state[1] = len + 1;
+    }
     const ST* row = token ? src + (int64_t)(*token) * d : src;
     const int64_t c0 = (int64_t)blockIdx.x * tile;
     const int64_t c1 = min64(d, c0 + tile);
@@ -218,13 +223,13 @@ int teal_decode_attention(const float* q, const void* k_cache, const void* v_cac
 }
 
 int teal_load_residual(const void* src, int src_dtype, const int* token, int64_t d, float* x, float* ss_out, int tile,
-                       cudaStream_t stream) {
+                       int* step_state, cudaStream_t stream) {
     TEAL_REQUIRE(src && x && d >= 1 && tile >= 1, "teal_load_residual: bad arguments");
     const int grid = (int)((d + tile - 1) / tile);
     if (src_dtype == TEAL_F32)
-        load_residual_kernel<float><<<grid, kThreads, 0, stream>>>((const float*)src, token, d, x, ss_out, tile);
+        load_residual_kernel<float><<<grid, kThreads, 0, stream>>>((const float*)src, token, d, x, ss_out, tile, step_state);
     else if (src_dtype == TEAL_BF16)
-        load_residual_kernel<uint16_t><<<grid, kThreads, 0, stream>>>((const uint16_t*)src, token, d, x, ss_out, tile);
+        load_residual_kernel<uint16_t><<<grid, kThreads, 0, stream>>>((const uint16_t*)src, token, d, x, ss_out, tile, step_state);
     else
         TEAL_REQUIRE(false, "teal_load_residual: unsupported dtype %d", src_dtype);
     return check_launch("teal_load_residual");

@@ -1,0 +1,104 @@
+"""CPU: the C-ABI library builds for sm_100a, loads, and exports exactly the
+entry points include/teal_b200.h declares; host-side logic that needs no GPU."""
+
+from __future__ import annotations
+
+import re
+import shutil
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+
+def header_functions():
+    text = (ROOT / "include" / "teal_b200.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|int64_t)\s+(teal_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2408_14690_b200 import _clib as C
+    L = C.lib()
+    declared = header_functions()
+    assert declared, "no declarations parsed"
+    assert sorted(C.EXPORTED) == declared
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.teal_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    from paper_2408_14690_b200 import _clib as C
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([cuobjdump, "--list-elf", str(C.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_invalid_args_raise_valueerror_without_gpu():
+    from paper_2408_14690_b200 import _clib as C
+    # argument validation happens before any CUDA call
+    with pytest.raises(ValueError, match="nseg"):
+        a = C.TealGemvArgs()
+        a.nseg = 0
+        import ctypes
+        C.check(C.lib().teal_fused_gemv(ctypes.byref(a), None))
+    with pytest.raises(ValueError, match="non-negative"):
+        C.call("teal_threshold", None, 0, 10, -1.0, None, None, None, None)
+
+
+def test_threshold_rounding_modes():
+    from paper_2408_14690_b200 import _runtime as RT
+    t = 0.3
+    rn, rd = RT.f32_round_nearest(t), RT.f32_round_down(t)
+    assert rn == float(np.float32(0.3)) and rn > t          # fl32(0.3) > 0.3
+    assert rd < t and np.float32(rd) == np.nextafter(np.float32(rn), np.float32(0))
+    assert RT.f32_round_down(0.5) == 0.5 and RT.f32_round_down(float("inf")) == float("inf")
+    # the fp64 compare |x| <= t of _skip_gemv equals the fp32 compare against RD32(t)
+    xs = np.array([np.float32(0.3), np.nextafter(np.float32(0.3), 0), 0.29999998], np.float32)
+    assert [abs(float(v)) <= t for v in xs] == [bool(abs(v) <= np.float32(rd)) for v in xs]
+
+
+def test_gemv_workspace_plan():
+    import torch
+    from paper_2408_14690_b200 import _runtime as RT
+    for m, n, dt in [(4096, 14336, torch.bfloat16), (14336, 4096, torch.bfloat16), (4096, 128256, torch.bfloat16),
+                     (512, 1408, torch.float32), (1, 1, torch.float32), (28672, 8192, torch.bfloat16)]:
+        wt = torch.empty(m, n, dtype=dt)
+        a = RT.single_gemv_args(wt, n, torch.empty(m), 0.5, torch.empty(n))
+        g, nws, ntk = RT.gemv_workspace(a)
+        tile = 512 if (dt == torch.bfloat16 and n % 16 == 0) else 256
+        tiles = -(-n // tile)
+        groups = tiles * (-(-m // 32))
+        assert 1 <= g <= groups and ntk == tiles and nws >= tiles * tile
+
+
+def test_traffic_model_matches_reference():
+    import paper_2408_14690_b200 as T
+    r = T.traffic_model(4096, 14336, 0.5)
+    assert r.weight_bytes_sparse == 117_440_512 and r.activation_bytes == 14336 * 4
+    assert T.traffic_model(8, 8, 0.0).weight_bytes_dense == 256
+    assert T.traffic_model(16, 16, 1.0).weight_bytes_sparse == 0.0
+    assert T.traffic_model(4096, 4096, 0.5, 0.5).weight_bytes_sparse == 4096 * 4096 * 0.25
+    with pytest.raises(ValueError):
+        T.traffic_model(0, 8, 0.5)
+    with pytest.raises(ValueError):
+        T.traffic_model(8, 8, 1.5)
+
+
+def test_gaussian_threshold_kat():
+    import paper_2408_14690_b200 as T
+    from conftest import golden
+    g = golden("theory")
+    for p, t in zip(g["p"], g["t"]):
+        assert T.gaussian_threshold(float(p)) == t
+
+
+def test_rng_stream_reproduces_reference_draws():
+    import paper_2408_14690_b200 as T
+    from oracle import actsparse_ref as R
+    a = T.sample_gaussian(T.RngStream(202), 1000, 1.0)
+    b = R.philox_generator(202, 0).standard_normal(1000, dtype=np.float32)
+    assert a.tobytes() == b.tobytes()
+    assert T.RngStream(5).child(1).seed == R.child_seed(5, 1)
