@@ -1,0 +1,477 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native TEAL decode hot path (BASELINE.json metric:
+"batch-1 decode tokens/sec & sparse-GEMV HBM GB/s at 0/40/50% sparsity").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (config 3 of BASELINE.json, the largest single-GPU decode config):
+Llama-3-8B random-init bf16 weights, batch-1 greedy decode, TEAL uniform
+50% sparsity with thresholds calibrated on the GPU (histograms of the four
+taps over 16 dense decode steps).  One "step" = one decoded token: the whole
+captured CUDA graph (residual load, 32 x [qkv | attention | o | gate-up |
+down], dense LM head, argmax).  Weights are 16 GB per step, far larger than
+L2, so no flush is needed between steps.
+
+Line keys beyond the base contract:
+  roofline      the fused gate/up sparse GEMV (the largest launch of a step),
+                algorithmic bytes (kept*n*2 over both segments + m*4 + n*4)
+                / its CUDA-event duration, against MEASURED_PEAKS.json (or
+                the profiling guide's fallback, stated in `peak_src`)
+  cpu_baseline  the oracle's C port of the reference `_skip_gemv`
+                (oracle/teal_oracle.c) on 1 host core, fp32 rows, on a
+                bounded sample (one layer's 7 projections + an LM-head slice)
+  sweep         decode tok/s at dense / 0 / 25 / 40 / 50 % and the per-shape
+                sparse-GEMV GB/s at 0 / 40 / 50 % (the metric's second half)
+  e2e           the same decode through SparseDecoder.step_token_host: H2D of
+                the input token from pinned memory and D2H of the argmax every
+                step, inside the timed region
+
+`--impl reference` times the reference CPU path (the oracle port of
+`_skip_gemv`, all host threads, fp32) on the same workload: each step is one
+layer's 7 projections at 50% plus an LM-head slice, extrapolated to a token.
+Multi-GPU: the 8B decode fits one GPU, so N>1 runs N independent replicas
+(weak scaling, no collective on the data path); `value` = N*K / max-rank time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "batch-1 decode tokens/sec & sparse-GEMV HBM GB/s at 0/40/50% sparsity"
+UNIT = "tokens/s"
+FALLBACK_HBM_GBS = 6650.0
+GEMV_SHAPES = {"q": (4096, 4096), "k": (1024, 4096), "v": (1024, 4096), "o": (4096, 4096),
+               "gate": (14336, 4096), "up": (14336, 4096), "down": (4096, 14336)}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--sparsity", type=float, default=0.5)
+    ap.add_argument("--levels", default="0,0.25,0.4,0.5")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the per-level / per-shape sweep")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    return ap.parse_args()
+
+
+def peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            for k in ("hbm_gbs", "hbm_GBs", "hbm"):
+                if k in d:
+                    return float(d[k]), "measured"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+# ---- clocks during the timed region ------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---- distributed plumbing --------------------------------------------------------
+def dist_setup():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v: float, ws: int) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def timed(fn, steps: int, ws: int):
+    """Device time (ms) of `steps` calls of fn, barrier + sync on both sides,
+    CUDA events on the current stream; max over ranks."""
+    import torch
+    barrier(ws)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    barrier(ws)
+    return max_over_ranks(a.elapsed_time(b), ws)
+
+
+# ---- CPU baseline (oracle port of the reference `_skip_gemv`) -----------------------
+def make_cpu_sample(threads: int, sparsity: float, seed: int = 5):
+    """Seconds per token of the reference CPU path, estimated from a bounded
+    sample: one Llama-3-8B layer's seven projections (fp32 input-major rows,
+    t = gaussian_threshold(s), x ~ N(0,1) as kernel.bench_gemv draws them) and
+    a 1/16 column slice of the dense LM head; token = 32 layers + 16 slices."""
+    import numpy as np
+    from oracle import cpu as OC
+    from paper_2408_14690_b200.theory import gaussian_threshold
+    g = np.random.default_rng(seed)
+    t = gaussian_threshold(sparsity) if sparsity > 0 else -1.0
+    mats = []
+    for name, (n, m) in GEMV_SHAPES.items():
+        mats.append((g.standard_normal((m, n), dtype=np.float32), g.standard_normal(m, dtype=np.float32), t))
+    lm_slice = 128256 // 16
+    mats.append((g.standard_normal((4096, lm_slice), dtype=np.float32), g.standard_normal(4096, dtype=np.float32), -1.0))
+
+    def one():
+        t0 = time.perf_counter()
+        for w, x, tt in mats[:7]:
+            OC.skip_gemv(x, w, tt, threads=threads)
+        t1 = time.perf_counter()
+        w, x, tt = mats[7]
+        OC.skip_gemv(x, w, tt, threads=threads)
+        t2 = time.perf_counter()
+        return 32 * (t1 - t0) + 16 * (t2 - t1)
+
+    return one
+
+
+def cpu_layer_sample(threads: int, sparsity: float, reps: int, seed: int = 5):
+    one = make_cpu_sample(threads, sparsity, seed)
+    one()  # warm-up (page-in)
+    return [one() for _ in range(reps)]
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU path on all host threads, rank 0 only."""
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import cpu as OC
+    threads = OC.max_threads()
+    one = make_cpu_sample(threads, args.sparsity)
+    for _ in range(args.warmup):  # each step is one bounded sample (layer + LM-head slice)
+        one()
+    samples = [one() for _ in range(args.steps)]
+    tok_s = 1.0 / statistics.median(samples)
+    sample = (f"per step: Llama-3-8B layer-0 q/k/v/o/gate/up/down at s={args.sparsity} (fp32 input-major, "
+              f"t=gaussian_threshold) + 1/16 LM-head slice dense; token time = 32 layers + 16 slices; "
+              f"attention excluded (<0.1% at this context)")
+    line = {"impl": "reference", "metric": METRIC, "value": round(tok_s, 4), "unit": UNIT,
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 / tok_s, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "llama3-8b batch-1 decode, TEAL uniform sparsity",
+                       "sparsity": args.sparsity, "batch": 1},
+            "cpu_baseline": {"value": round(tok_s, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(tok_s, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- our arm -----------------------------------------------------------------------
+def capture_steps(dec):
+    dec.reset()
+    dec.capture(from_token=True)
+    dec.reset()
+
+
+def decode_tok_s(D, W, thr, steps, warmup, ws):
+    import torch
+    dec = D.SparseDecoder(W, thr)
+    capture_steps(dec)
+    for _ in range(warmup):
+        dec.replay()
+    ms = timed(dec.replay, steps, ws)
+    n = dec.launches_per_step()
+    del dec
+    torch.cuda.empty_cache()
+    return steps * 1e3 / ms, ms / steps, n
+
+
+def gate_up_roofline(D, C, W, thr, reps: int = 20):
+    """Time the fused gate/up launch of every layer back to back (one CUDA
+    graph of n_layers launches, weights 7.3 GB > L2) and report its achieved
+    GB/s on algorithmic bytes."""
+    import ctypes
+    import torch
+    spec = W.spec
+    dec = D.SparseDecoder(W, thr)
+    dec.reset()
+    dec.token.fill_(1)
+    dec.step_token()  # a realistic residual state in dec.x / dec.ss
+    torch.cuda.synchronize()
+    kept = torch.zeros(spec.n_layers, 2, dtype=torch.int64, device=dec.device)
+    L = C.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    for l, (_, _, gu, _) in enumerate(dec.layer_args):
+        a = C.TealGemvArgs.from_buffer_copy(gu)
+        a.seg[0].kept = kept[l, 0].data_ptr()
+        a.seg[1].kept = kept[l, 1].data_ptr()
+        C.check(L.teal_fused_gemv(ctypes.byref(a), s))
+    torch.cuda.synchronize()
+    kept_h = kept.cpu().tolist()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(st):
+        with torch.cuda.graph(g, stream=st):
+            for (_, _, gu, _) in dec.layer_args:
+                C.check(L.teal_fused_gemv(ctypes.byref(gu), st.cuda_stream))
+    torch.cuda.current_stream().wait_stream(st)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in evs:
+        a.record()
+        g.replay()
+        b.record()
+    torch.cuda.synchronize()
+    per_launch_us = statistics.median(a.elapsed_time(b) for a, b in evs) * 1e3 / spec.n_layers
+    d, f = spec.d_model, spec.d_ff
+    esz = W.layers[0].wgu.element_size()
+    algo = [(kg + ku) * f * esz + d * 4 + f * 4 for kg, ku in kept_h]
+    algo_mean = sum(algo) / len(algo)
+    kept_frac = sum(kg + ku for kg, ku in kept_h) / (2 * d * spec.n_layers)
+    del dec, g
+    torch.cuda.empty_cache()
+    return {"per_launch_us": per_launch_us, "algo_bytes": algo_mean, "kept_frac": kept_frac,
+            "gbs": algo_mean / (per_launch_us * 1e-6) / 1e9}
+
+
+def gemv_sweep(levels, reps: int = 20):
+    """Sparse-GEMV GB/s per Llama-3-8B projection shape (config 2): rotating
+    weight pool > 3x L2, graph of back-to-back launches, CUDA events."""
+    import torch
+    import paper_2408_14690_b200 as T
+    from paper_2408_14690_b200 import _runtime as RT
+    from paper_2408_14690_b200.tensor import _gemv
+    dev = torch.device("cuda", torch.cuda.current_device())
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    gen = torch.Generator(device=dev).manual_seed(0)
+    out = {}
+    for name, (n, m) in GEMV_SHAPES.items():
+        nbytes = n * m * 2
+        copies = max(2, math.ceil(3 * l2 / nbytes))
+        pool = [T.Matrix.from_device(torch.randn(m, n, device=dev, generator=gen).to(torch.bfloat16))
+                for _ in range(copies)]
+        x = torch.randn(m, device=dev, generator=gen)
+        y = torch.empty(n, device=dev)
+        row = {}
+        for s in levels:
+            t = T.gaussian_threshold(s)
+            t32 = RT.f32_round_down(t) if s > 0 else float("-inf")
+            kept = int((~(x.abs().double() <= t)).sum().item()) if s > 0 else m
+            inner = max(copies, 8)
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                for i in range(3):
+                    _gemv(pool[i % copies], x, t32, out=y)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    for i in range(inner):
+                        _gemv(pool[i % copies], x, t32, out=y)
+            torch.cuda.current_stream().wait_stream(st)
+            g.replay()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+            torch.cuda.synchronize()
+            for a, b in evs:
+                a.record()
+                g.replay()
+                b.record()
+            torch.cuda.synchronize()
+            us = statistics.median(a.elapsed_time(b) for a, b in evs) * 1e3 / inner
+            algo = kept * n * 2 + m * 4 + n * 4
+            row[str(s)] = {"us": round(us, 2), "gbs": round(algo / (us * 1e-6) / 1e9, 1)}
+            del g
+        out[name] = row
+        del pool
+        torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_setup()
+    import paper_2408_14690_b200 as T  # noqa: F401  (loads lib/libteal_b200.so; no CPU fallback)
+    from paper_2408_14690_b200 import _clib as C
+    from paper_2408_14690_b200 import decode as D
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device")
+    peak, peak_src = peak_hbm()
+    spec = D.LLAMA3_8B
+    W = D.random_weights(spec, torch.bfloat16, seed=rank)
+    hists = D.calibrate_histograms(W, n_tokens=16, seed=1000 + rank)
+    levels = sorted({float(v) for v in args.levels.split(",")} | {args.sparsity})
+    thr = {s: D.uniform_thresholds(hists, spec.n_layers, s) for s in levels}
+    torch.cuda.synchronize()
+
+    # headline: K timed decode steps at the target sparsity, clocks sampled
+    dec = D.SparseDecoder(W, thr[args.sparsity])
+    capture_steps(dec)
+    for _ in range(args.warmup):
+        dec.replay()
+    with ClockSampler(local) as clk:
+        ms = timed(dec.replay, args.steps, ws)
+    value = ws * args.steps * 1e3 / ms
+    launches = dec.launches_per_step() * args.steps
+
+    # e2e: same steps through host buffers (H2D token in, D2H argmax out per step)
+    dec.reset()
+    tin = torch.ones(args.steps, 1, dtype=torch.int32).pin_memory()
+    tout = torch.zeros(args.steps, 1, dtype=torch.int32).pin_memory()
+    for i in range(args.warmup):
+        dec.step_token_host(tin[i % args.steps], tout[i % args.steps])
+    it = iter(range(args.steps))
+    ms_e2e = timed(lambda: (lambda i: dec.step_token_host(tin[i], tout[i]))(next(it)), args.steps, ws)
+    e2e = ws * args.steps * 1e3 / ms_e2e
+    del dec
+    torch.cuda.empty_cache()
+
+    roof = gate_up_roofline(D, C, W, thr[args.sparsity])
+    sweep = None
+    if not args.no_sweep:
+        dense_tok, dense_ms, _ = decode_tok_s(D, W, None, max(20, args.steps // 2), 3, ws)
+        dec_rows = {"dense": round(dense_tok, 2)}
+        for s in levels:
+            tok, _, _ = decode_tok_s(D, W, thr[s], max(20, args.steps // 2), 3, ws)
+            dec_rows[str(s)] = round(tok, 2)
+        sweep = {"decode_tok_s": dec_rows,
+                 "speedup_vs_dense": {k: round(v / dense_tok, 3) for k, v in dec_rows.items() if k != "dense"},
+                 "dense_weight_gb_per_token": round(sum(spec.weight_bytes(2).values()) / 1e9, 3),
+                 "dense_hbm_frac": round(dense_tok * sum(spec.weight_bytes(2).values()) / 1e9 / peak, 3)}
+        del W
+        torch.cuda.empty_cache()
+        sweep["gemv_gbs"] = gemv_sweep([0.0, 0.4, 0.5])
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        samples = cpu_layer_sample(1, args.sparsity, reps=args.cpu_reps)
+        cpu = {"value": round(1.0 / statistics.median(samples), 4), "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": (f"oracle C port of reference _skip_gemv (kernel.py:30-44), 1 thread, fp32: Llama-3-8B "
+                          f"layer-0 7 projections at s={args.sparsity} + 1/16 LM-head slice, x{args.cpu_reps} reps; "
+                          f"token = 32 layers + 16 slices; host has {os.cpu_count()} cores")}
+
+    traffic = None
+    tp = ROOT / "profiles" / "gate_up_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "llama3-8b random-init batch-1 decode, TEAL uniform calibrated sparsity",
+                       "sparsity": args.sparsity, "batch": 1, "weights": "bf16 input-major",
+                       "parallelism": "replicas" if ws > 1 else "single",
+                       "l2": "inputs larger than L2 (15 GB of weights per step)"},
+            "roofline": {"bound": "hbm", "kernel": "teal gemv_tma_kernel (fused gate/up, SiLU epilogue)",
+                         "achieved": round(roof["gbs"], 1), "peak": peak, "peak_src": peak_src, "unit": "GB/s",
+                         "frac": round(roof["gbs"] / peak, 4), "traffic": traffic,
+                         "algo_bytes_per_launch": int(roof["algo_bytes"]),
+                         "us_per_launch": round(roof["per_launch_us"], 2),
+                         "kept_frac": round(roof["kept_frac"], 4),
+                         "share_of_step": round(roof["per_launch_us"] * spec.n_layers / (ms / args.steps * 1e3), 3)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 4},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -382,6 +382,14 @@ class SparseDecoder:
             self._launch_step(RT.stream_handle(), from_token=True)
         return self.token
 
+    def step_token_host(self, tok_in: torch.Tensor, tok_out: torch.Tensor) -> None:
+        """End-to-end step through host buffers: H2D copy of the input token
+        (pinned int32 [1]), one decode step, D2H copy of the argmax token into
+        ``tok_out`` (pinned int32 [1]).  Stream-ordered, no host sync."""
+        self.token.copy_(tok_in, non_blocking=True)
+        self.step_token()
+        tok_out.copy_(self.token, non_blocking=True)
+
     def capture(self, from_token: bool = True) -> torch.cuda.CUDAGraph:
         """Capture one step into a CUDA graph (replayed by step_token / replay())."""
         s = torch.cuda.Stream(device=self.device)
@@ -396,3 +404,57 @@ class SparseDecoder:
 
     def replay(self) -> None:
         self.graph.replay()
+
+
+# tap of each projection's input (model.py:39-56, MATRIX_TAP)
+PROJ_TAP = {"q": "pre_attn", "k": "pre_attn", "v": "pre_attn", "o": "attn_out",
+            "gate": "pre_mlp", "up": "pre_mlp", "down": "mlp_inter"}
+
+
+def calibrate_histograms(weights: DecoderWeights, n_tokens: int = 16, seed: int = 0,
+                         bins: int | None = None, hi_std_multiple: float | None = None):
+    """GPU-side calibration of the decode engine (model.py:268-294 restated for
+    the KV-cache decode): run ``n_tokens`` dense decode steps on random tokens
+    with the four taps captured, and bin each (layer, tap) vector on the GPU
+    (``teal_hist_record``).  ``hi`` = HI_STD_MULTIPLE * std of the first
+    step's tap, as the reference takes it from the first calibration sequence
+    (model.py:286-291).  Returns {(layer, tap): ActivationHistogram}."""
+    from .sparsifier import DEFAULT_BIN_COUNT, HI_STD_MULTIPLE, ActivationHistogram
+    bins = bins or DEFAULT_BIN_COUNT
+    mult = hi_std_multiple or HI_STD_MULTIPLE
+    spec = weights.spec
+    if not spec.vocab:
+        raise ValueError("token calibration needs an embedding (vocab > 0)")
+    dec = SparseDecoder(weights, None, taps=True)
+    dec.reset()
+    g = torch.Generator(device=dec.device).manual_seed(seed)
+    toks = torch.randint(0, spec.vocab, (n_tokens,), device=dec.device, generator=g, dtype=torch.int32)
+    hists = {}
+    for i in range(n_tokens):
+        dec.token.copy_(toks[i:i + 1])
+        dec.step_token()
+        for tap, h in dec.taps.h.items():
+            for l in range(spec.n_layers):
+                key = (l, tap)
+                if key not in hists:
+                    hi = mult * float(h[l].std(unbiased=False))
+                    hists[key] = ActivationHistogram.empty(f"L{l}.{tap}", bins, hi if hi > 0 else 1.0)
+                hists[key].record(h[l])
+    del dec
+    return hists
+
+
+def uniform_thresholds(hists, n_layers: int, level: float) -> list[list[float]]:
+    """Per-layer thresholds of a uniform config (greedy.py:130-134 with
+    resolve_config, model.py:253-265): every projection at ``level``."""
+    out = []
+    cache = {}
+    for l in range(n_layers):
+        row = []
+        for p in PROJ:
+            key = (l, PROJ_TAP[p])
+            if key not in cache:
+                cache[key] = hists[key].threshold(level)
+            row.append(cache[key])
+        out.append(row)
+    return out
