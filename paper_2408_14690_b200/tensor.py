@@ -235,3 +235,42 @@ def sample_laplace(rng: RngStream, n: int, scale: float) -> np.ndarray:
     if not scale > 0:
         raise ValueError(f"scale must be positive, got {scale}")
     return (rng.next_generator().laplace(0.0, 1.0, size=n) * scale).astype(np.float32)
+
+
+# ---- weight file TEALW1 (tensor.py:197-235), byte-compatible ----------------------
+#
+# Header b"TEALW1 <rows> <cols> <layout>\n" then rows*cols little-endian f32 in
+# logical row-major order whatever the layout; the round trip is bit-exact, so
+# weights written by the reference CLI load straight into HBM here.
+
+def write_matrix(fh, w: Matrix) -> None:
+    fh.write(f"{WEIGHT_MAGIC} {w.rows} {w.cols} {w.layout.value}\n".encode("ascii"))
+    fh.write(np.ascontiguousarray(w.to_2d(), dtype="<f4").tobytes(order="C"))
+
+
+def read_matrix(fh) -> Matrix:
+    header = fh.readline().decode("ascii", errors="replace").strip()
+    parts = header.split()
+    if len(parts) != 4 or parts[0] != WEIGHT_MAGIC:
+        raise ValueError(f"bad weight header: {header!r}")
+    rows, cols = int(parts[1]), int(parts[2])
+    try:
+        layout = Layout(parts[3])
+    except ValueError:
+        raise ValueError(f"unknown layout tag {parts[3]!r} in weight header") from None
+    nbytes = rows * cols * 4
+    payload = fh.read(nbytes)
+    if len(payload) != nbytes:
+        raise ValueError(f"truncated weight payload: expected {nbytes} bytes, got {len(payload)}")
+    arr = np.frombuffer(payload, dtype="<f4").astype(np.float32).reshape(rows, cols)
+    return Matrix.from_2d(arr, layout)
+
+
+def save_matrix(path, w: Matrix) -> None:
+    with open(path, "wb") as fh:
+        write_matrix(fh, w)
+
+
+def load_matrix(path) -> Matrix:
+    with open(path, "rb") as fh:
+        return read_matrix(fh)
