@@ -189,6 +189,113 @@ int teal_load_residual(const void* src, int src_dtype, const int* token, int64_t
 int teal_argmax(const float* logits, int64_t n, int* out_token,
                 float* ws, uint32_t* tickets, cudaStream_t stream);
 
+
+/* ---- persistent decode step (one launch per token) ----------------------
+ *
+ * Replaces the per-projection launches of a decode step (the seven
+ * `gated(name, a) @ W.T` products of model._forward, model.py:158-198, plus
+ * attention, residual load, LM head and argmax) with ONE persistent
+ * cooperative launch: every CTA pulls work units from a device queue in
+ * topological order and waits on per-dependency counters (no grid barrier,
+ * no host sync).  Weights are stored TILED input-major: a group's output
+ * columns are cut into tiles of TEAL_STEP_TW columns and tile t is the
+ * contiguous block w[t][i][0..TW) over input channels i (element (out
+ * t*TW + c, in i) = w[(t*m + i)*TW + c]); a kept channel streams one
+ * contiguous TW-column row chunk per tile.  Each tile carries two column
+ * halves with their own thresholds (gate | up interleaved for the MLP).
+ * A GEMV unit = (group, tile, K-range); K-split tiles are finished by the
+ * last-arriving unit, summing partials in split order (deterministic).  */
+#define TEAL_STEP_TW 256
+#define TEAL_UNIT_LOAD 0
+#define TEAL_UNIT_GEMV 1
+#define TEAL_UNIT_ATTN 2
+
+#define TEAL_SEPI_STORE 0    /* y[col] = v                                   */
+#define TEAL_SEPI_RESID 1    /* resid[col] += v ; ss_out[tile] = sum resid^2 */
+#define TEAL_SEPI_SILU 2     /* inter[t*TW/2 + c] = silu(lo_c) * hi_c         */
+#define TEAL_SEPI_QKV 3      /* q -> rope -> q_out ; k -> rope -> k cache ; v -> v cache */
+#define TEAL_SEPI_LOGITS 4   /* y[col] = v ; per-tile argmax candidate; last tile -> token */
+
+typedef struct teal_step_tile {
+    float t_lo, t_hi;        /* keep iff !(|h| <= t); -INFINITY = dense      */
+    int seg_lo, seg_hi;      /* debug segment of each half (0..2)            */
+    int first_lo, first_hi;  /* 1 if this tile is the first of its segment  */
+    int sig0, sig1;          /* counters [sig0, sig1] += 1 on finalize (sig0 < 0: none) */
+} teal_step_tile;
+
+typedef struct teal_step_group {
+    const void* w;           /* tiled weights [ntiles][m][TW]               */
+    const float* col_scale;  /* int8 rows: per-column scale [ntiles*TW]      */
+    const teal_step_tile* tiles;  /* [ntiles]                               */
+    const float* x;          /* input vector [m] (written earlier in the step) */
+    const float* gain;       /* PRO_RMSNORM gain [m]                         */
+    const float* ss;         /* PRO_RMSNORM: sum-of-squares partials [nss]   */
+    float* partials;         /* [ntiles][nsplit][TW]                          */
+    unsigned* tickets;       /* [ntiles], zero, self-resetting               */
+    float* y;                /* STORE / LOGITS output [n]                    */
+    float* resid;            /* RESID residual stream [n]                    */
+    float* ss_out;           /* RESID: [ntiles] partial sums of squares       */
+    float* inter;            /* SILU output [ntiles*TW/2]                    */
+    float* q_out;            /* QKV                                          */
+    void* k_cache;
+    void* v_cache;
+    const float* rope_cos;   /* nullable [max_seq][hd/2]                      */
+    const float* rope_sin;
+    float* dbg_h;            /* nullable: prologue h [m] (tile-0 units)      */
+    uint32_t* dbg_bits[3];   /* nullable: keep bits per segment [ceil(m/32)] */
+    unsigned long long* kept[3];  /* nullable: kept channels per segment    */
+    int64_t max_seq;
+    int m, n, ntiles, nsplit;
+    int prologue, nss;
+    float eps;
+    int epilogue;
+    int nq, nkv, head_dim, kv_dtype;
+    int pad_;
+} teal_step_group;
+
+typedef struct teal_step_attn {
+    const float* q;          /* [H*hd]                                       */
+    const void* k_cache;     /* [KVH][max_seq][hd]                            */
+    const void* v_cache;
+    float* ctx;              /* [H*hd]                                       */
+    float* partials;         /* [KVH][nchunks][G*hd + 2G]                    */
+    unsigned* tickets;       /* [KVH]                                        */
+    int64_t max_seq;
+    int H, KVH, hd, kv_dtype;
+    int chunk, nchunks;
+    int sig_base;            /* counter sig_base + g += 1 when group g's ctx is final */
+    int pad_;
+} teal_step_attn;
+
+typedef struct teal_step_unit {
+    int kind, group, tile, split, r0, r1, dep, target;
+} teal_step_unit;
+
+typedef struct teal_step_plan {
+    const teal_step_group* groups;   /* device arrays */
+    const teal_step_attn* attns;
+    const teal_step_unit* units;
+    int* counters;                   /* [ncounters] zero; reset at the end of every launch */
+    unsigned* ctrl;                  /* [4] zero: queue head, exit count */
+    const void* emb;                 /* LOAD: embedding [vocab][d] (NULL: x_in) */
+    const float* x_in;               /* LOAD: hidden row [d] when emb == NULL  */
+    const int* token;                /* LOAD: token id (device)                */
+    float* x;                        /* residual stream [d]                    */
+    float* ss;                       /* [d / TW] partial sums of squares       */
+    int* state;                      /* {pos, len}: LOAD sets pos = len, len += 1 */
+    float* cand_v;                   /* LOGITS: per-tile argmax candidates     */
+    int* cand_i;
+    int* token_out;                  /* LOGITS: argmax token                   */
+    unsigned* lm_done;               /* LOGITS: tiles finished (self-resetting) */
+    int nunits, ncounters;
+    int d, emb_dtype;
+    int w_dtype, ctas;               /* ctas <= 0: occupancy x SMs             */
+} teal_step_plan;
+
+/* CTAs per SM the step kernel runs at for a weight dtype (for sizing). */
+int teal_step_ctas_per_sm(int w_dtype);
+int teal_step_launch(const teal_step_plan* plan, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

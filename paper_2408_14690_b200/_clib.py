@@ -70,6 +70,8 @@ _SIGNATURES = [
                                              ctypes.c_int, c_vp]),
     ("teal_load_residual", ctypes.c_int, [c_vp, ctypes.c_int, c_vp, c_i64, c_vp, c_vp, ctypes.c_int, c_vp, c_vp]),
     ("teal_argmax", ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    ("teal_step_ctas_per_sm", ctypes.c_int, [ctypes.c_int]),
+    ("teal_step_launch", ctypes.c_int, [c_vp, c_vp]),
 ]
 
 EXPORTED = tuple(name for name, _, _ in _SIGNATURES)

@@ -1,0 +1,461 @@
+"""Persistent batch-1 decode engine: ONE cooperative sm_100a launch per token
+(``teal_step_launch``, csrc/teal_step.cu).
+
+Same decode-step semantics as :class:`.decode.SparseDecoder` (the
+reference's ``_forward`` for one new position against a KV cache,
+pkg/src/actsparse/model.py:158-198) but scheduled as a dependency-driven
+work queue instead of 5 launches per layer, so the 148 SMs stream weights
+without launch gaps or grid-wide barriers.
+
+Weights are re-laid out once into the TILED input-major format the kernel
+streams (``pack_tiled`` / ``pack_gate_up``): for a group with output columns
+cut into tiles of TW = 256, tile t is the contiguous block ``[m][TW]`` so a
+kept input channel reads one contiguous 512-byte (bf16) row chunk per tile.
+The MLP tile interleaves 128 gate and 128 up columns so the SiLU(gate)*up
+epilogue stays inside one tile.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _clib as C
+from . import _runtime as RT
+from .decode import PROJ, DecoderWeights, StepTaps, _t32
+
+TW = 256
+TH = TW // 2
+UNIT_LOAD, UNIT_GEMV, UNIT_ATTN = 0, 1, 2
+SEPI_STORE, SEPI_RESID, SEPI_SILU, SEPI_QKV, SEPI_LOGITS = 0, 1, 2, 3, 4
+
+c_i64, c_vp, c_f, c_i = ctypes.c_int64, ctypes.c_void_p, ctypes.c_float, ctypes.c_int
+
+
+class StepTile(ctypes.Structure):
+    _fields_ = [("t_lo", c_f), ("t_hi", c_f), ("seg_lo", c_i), ("seg_hi", c_i),
+                ("first_lo", c_i), ("first_hi", c_i), ("sig0", c_i), ("sig1", c_i)]
+
+
+class StepGroup(ctypes.Structure):
+    _fields_ = [("w", c_vp), ("col_scale", c_vp), ("tiles", c_vp), ("x", c_vp), ("gain", c_vp), ("ss", c_vp),
+                ("partials", c_vp), ("tickets", c_vp), ("y", c_vp), ("resid", c_vp), ("ss_out", c_vp),
+                ("inter", c_vp), ("q_out", c_vp), ("k_cache", c_vp), ("v_cache", c_vp), ("rope_cos", c_vp),
+                ("rope_sin", c_vp), ("dbg_h", c_vp), ("dbg_bits", c_vp * 3), ("kept", c_vp * 3),
+                ("max_seq", c_i64), ("m", c_i), ("n", c_i), ("ntiles", c_i), ("nsplit", c_i),
+                ("prologue", c_i), ("nss", c_i), ("eps", c_f), ("epilogue", c_i),
+                ("nq", c_i), ("nkv", c_i), ("head_dim", c_i), ("kv_dtype", c_i), ("pad_", c_i)]
+
+
+class StepAttn(ctypes.Structure):
+    _fields_ = [("q", c_vp), ("k_cache", c_vp), ("v_cache", c_vp), ("ctx", c_vp), ("partials", c_vp),
+                ("tickets", c_vp), ("max_seq", c_i64), ("H", c_i), ("KVH", c_i), ("hd", c_i), ("kv_dtype", c_i),
+                ("chunk", c_i), ("nchunks", c_i), ("sig_base", c_i), ("pad_", c_i)]
+
+
+class StepPlan(ctypes.Structure):
+    _fields_ = [("groups", c_vp), ("attns", c_vp), ("units", c_vp), ("counters", c_vp), ("ctrl", c_vp),
+                ("emb", c_vp), ("x_in", c_vp), ("token", c_vp), ("x", c_vp), ("ss", c_vp), ("state", c_vp),
+                ("cand_v", c_vp), ("cand_i", c_vp), ("token_out", c_vp), ("lm_done", c_vp),
+                ("nunits", c_i), ("ncounters", c_i), ("d", c_i), ("emb_dtype", c_i), ("w_dtype", c_i), ("ctas", c_i)]
+
+
+_BOUND = False
+
+
+def _bind():
+    global _BOUND
+    if not _BOUND:
+        L = C.lib()
+        L.teal_step_launch.restype = ctypes.c_int
+        L.teal_step_launch.argtypes = [ctypes.POINTER(StepPlan), c_vp]
+        L.teal_step_ctas_per_sm.restype = ctypes.c_int
+        L.teal_step_ctas_per_sm.argtypes = [c_i]
+        _BOUND = True
+    return C.lib()
+
+
+# ---- tiled weight layout --------------------------------------------------------
+
+def pack_tiled(w_in_major: torch.Tensor, tw: int = TW) -> torch.Tensor:
+    """[m, n] input-major -> [ceil(n/tw), m, tw] (zero-padded columns)."""
+    m, n = w_in_major.shape
+    nt = -(-n // tw)
+    out = torch.zeros(nt, m, tw, dtype=w_in_major.dtype, device=w_in_major.device)
+    for t in range(nt):
+        c1 = min(n, (t + 1) * tw)
+        out[t, :, : c1 - t * tw] = w_in_major[:, t * tw: c1]
+    return out
+
+
+def pack_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor, tw: int = TW) -> torch.Tensor:
+    """gate/up [m, f] each -> [ceil(f/(tw/2)), m, tw]: tile t = gate cols
+    [t*tw/2, (t+1)*tw/2) | up cols of the same range."""
+    m, f = w_gate.shape
+    th = tw // 2
+    nt = -(-f // th)
+    out = torch.zeros(nt, m, tw, dtype=w_gate.dtype, device=w_gate.device)
+    for t in range(nt):
+        c1 = min(f, (t + 1) * th)
+        out[t, :, : c1 - t * th] = w_gate[:, t * th: c1]
+        out[t, :, th: th + c1 - t * th] = w_up[:, t * th: c1]
+    return out
+
+
+def _splits(m: int, rows: int) -> list[tuple[int, int]]:
+    """K-ranges of at most `rows` rows (multiples of 32, balanced)."""
+    n = max(1, -(-m // rows))
+    per = -(-(-(-m // n)) // 32) * 32
+    out, r = [], 0
+    while r < m:
+        out.append((r, min(m, r + per)))
+        r += per
+    return out
+
+
+class StepDecoder:
+    """TEAL decode for one sequence with one persistent launch per token.
+
+    Same constructor arguments and step API as :class:`.decode.SparseDecoder`
+    (thresholds per layer in the order q,k,v,o,gate,up,down; None or -inf =
+    dense for that projection)."""
+
+    def __init__(self, weights: DecoderWeights, thresholds=None, kv_dtype=None, device=None,
+                 taps: bool = False, rows_per_unit: int = 512, attn_chunk: int = 256, ctas: int = 0,
+                 count_kept: bool = False):
+        self.w = weights
+        spec = self.spec = weights.spec
+        dev = self.device = device or RT.require_cuda()
+        _bind()
+        d, f, hd = spec.d_model, spec.d_ff, spec.head_dim
+        nq, nkv, L = spec.n_q, spec.n_kv, spec.n_layers
+        G = spec.n_heads // spec.n_kv_heads
+        if d % TW or nq % TW or nkv % TW or TW % hd or f % TH:
+            raise ValueError(f"StepDecoder needs d, n_q, n_kv multiples of {TW}, head_dim | {TW}, d_ff multiple of {TH}")
+        if G > 8 or hd > 128 or G * hd > 1024:
+            raise ValueError("StepDecoder attention supports <= 8 q heads per kv head and head_dim <= 128")
+        if attn_chunk > 256:
+            raise ValueError("attn_chunk must be <= 256")
+        self.rows_per_unit = min(1024, max(32, rows_per_unit // 32 * 32))
+        self.kv_dtype = kv_dtype or weights.dtype
+        self.w_dtype = weights.dtype
+        f32 = dict(device=dev, dtype=torch.float32)
+        # tiled weights
+        self.tw = []
+        for lw in weights.layers:
+            self.tw.append(dict(qkv=pack_tiled(lw.wqkv), o=pack_tiled(lw.wo),
+                                gu=pack_gate_up(lw.wgu[:, :f], lw.wgu[:, f:]), down=pack_tiled(lw.wdown)))
+        self.lm_t = pack_tiled(weights.lm_head) if spec.vocab else None
+        # activations / state
+        self.x = torch.zeros(d, **f32)
+        self.x_in = torch.zeros(d, **f32)
+        self.ss = torch.zeros(d // TW, **f32)
+        self.q = torch.zeros(nq, **f32)
+        self.ctx = torch.zeros(nq, **f32)
+        self.inter = torch.zeros(f, **f32)
+        self.state = torch.zeros(2, device=dev, dtype=torch.int32)
+        self.token = torch.zeros(1, device=dev, dtype=torch.int32)
+        self.logits = torch.zeros(max(spec.vocab, 1), **f32)
+        self.kcache = torch.zeros(L, spec.n_kv_heads, spec.max_seq, hd, device=dev, dtype=self.kv_dtype)
+        self.vcache = torch.zeros_like(self.kcache)
+        if spec.rope_theta is not None:
+            inv = 1.0 / (spec.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.float64) / hd))
+            ang = torch.arange(spec.max_seq, dtype=torch.float64)[:, None] * inv[None, :]
+            self.rope_cos = torch.cos(ang).float().to(dev).contiguous()
+            self.rope_sin = torch.sin(ang).float().to(dev).contiguous()
+        else:
+            self.rope_cos = self.rope_sin = None
+        self.attn_chunk = attn_chunk
+        self.nchunks = -(-spec.max_seq // attn_chunk)
+        self.taps = StepTaps() if taps else None
+        if taps:
+            for tap, dim in (("pre_attn", d), ("attn_out", nq), ("pre_mlp", d), ("mlp_inter", f)):
+                self.taps.h[tap] = torch.zeros(L, dim, **f32)
+            for p, (_, m_in) in spec.proj_shapes().items():
+                self.taps.bits[p] = torch.zeros(L, (m_in + 31) // 32, device=dev, dtype=torch.int32)
+            self.taps.kept = torch.zeros(L, 7, device=dev, dtype=torch.int64)
+        # kept-channel counters accumulated over every step (for algorithmic bytes)
+        self.kept = self.taps.kept if taps else (torch.zeros(L, 7, device=dev, dtype=torch.int64) if count_kept else None)
+        self.ctas = ctas
+        self._build(thresholds)
+        self.graph = None
+
+    # -- plan -----------------------------------------------------------------
+    def _build(self, thresholds):
+        spec, dev = self.spec, self.device
+        d, f, hd, L = spec.d_model, spec.d_ff, spec.head_dim, spec.n_layers
+        nq, nkv, KVH = spec.n_q, spec.n_kv, spec.n_kv_heads
+        G = spec.n_heads // KVH
+        thr = [[None] * 7 for _ in range(L)] if thresholds is None else [list(t) for t in thresholds]
+        if len(thr) != L or any(len(t) != 7 for t in thr):
+            raise ValueError(f"need {L} per-layer threshold lists of 7 (q,k,v,o,gate,up,down)")
+        self.thresholds = thr
+        R = self.rows_per_unit
+        nt_qkv, nt_o, nt_gu, nt_dn = (nq + 2 * nkv) // TW, d // TW, f // TH, d // TW
+        sp_qkv = _splits(d, R)
+        sp_o = [(g * G * hd, (g + 1) * G * hd) for g in range(KVH)]
+        sp_gu = _splits(d, R)
+        KC = max(TH, (R // TH) * TH)                      # down K-chunk: whole gate/up tiles
+        sp_dn = [(r, min(f, r + KC)) for r in range(0, f, KC)]
+        # counters
+        per_layer = 2 * KVH + 1 + len(sp_dn) + 1
+        self.ncounters = 1 + per_layer * L
+
+        def cbase(l):
+            b = 1 + per_layer * l
+            return dict(attn=b, odep=b + KVH, odone=b + 2 * KVH, gu=b + 2 * KVH + 1,
+                        down=b + 2 * KVH + 1 + len(sp_dn))
+
+        # workspaces (shared by the same group kind across layers)
+        self.ws = {
+            "qkv": torch.zeros(nt_qkv * len(sp_qkv) * TW, device=dev),
+            "o": torch.zeros(nt_o * len(sp_o) * TW, device=dev),
+            "gu": torch.zeros(nt_gu * len(sp_gu) * TW, device=dev),
+            "down": torch.zeros(nt_dn * len(sp_dn) * TW, device=dev),
+        }
+        self.tk = {k: torch.zeros(4096, device=dev, dtype=torch.int32) for k in ("qkv", "o", "gu", "down", "lm", "attn")}
+        rec = G * hd + 2 * G
+        self.ws["attn"] = torch.zeros(KVH * self.nchunks * rec, device=dev)
+
+        groups, attns, units, tiles_all = [], [], [], []
+        T = self.taps
+        K = self.kept
+
+        def tiles_tensor(meta):
+            arr = (StepTile * len(meta))(*meta)
+            t = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(dev)
+            tiles_all.append(t)
+            return t
+
+        def tile(tlo, thi, slo, shi, flo, fhi, s0, s1):
+            return StepTile(tlo, thi, slo, shi, flo, fhi, s0, s1)
+
+        units.append((UNIT_LOAD, 0, 0, 0, 0, 0, -1, 0))
+        for l, t in enumerate(thr):
+            cb = cbase(l)
+            tw = self.tw[l]
+            lw = self.w.layers[l]
+            kc, vc = self.kcache[l], self.vcache[l]
+            dep_in = (0, 1) if l == 0 else (cbase(l - 1)["down"], nt_dn)
+            # --- qkv
+            meta, feeds = [], [0] * KVH
+            for ti in range(nt_qkv):
+                c0, c1 = ti * TW, ti * TW + TW - 1
+                seg = 0 if c0 < nq else (1 if c0 < nq + nkv else 2)
+                first = c0 in (0, nq, nq + nkv)
+                if seg == 0:
+                    g0, g1 = (c0 // hd) // G, (c1 // hd) // G
+                else:
+                    off = nq if seg == 1 else nq + nkv
+                    g0, g1 = (c0 - off) // hd, (c1 - off) // hd
+                for gg in range(g0, g1 + 1):
+                    feeds[gg] += 1
+                tv = _t32(t[seg])
+                meta.append(tile(tv, tv, seg, seg, int(first), int(first), cb["attn"] + g0, cb["attn"] + g1))
+            gq = self._group(tw["qkv"], tiles_tensor(meta), m=d, n=nq + 2 * nkv, nsplit=len(sp_qkv),
+                             x=self.x, gain=lw.rms_attn, prologue=C.PRO_RMSNORM, ws="qkv", epilogue=SEPI_QKV,
+                             q_out=self.q, k_cache=kc, v_cache=vc,
+                             dbg=(T.h["pre_attn"][l] if T else None,
+                                  [T.bits[p][l] for p in ("q", "k", "v")] if T else None,
+                                  [K[l, PROJ.index(p)] for p in ("q", "k", "v")] if K is not None else None))
+            gi = len(groups)
+            groups.append(gq)
+            for ti in range(nt_qkv):
+                for s, (r0, r1) in enumerate(sp_qkv):
+                    units.append((UNIT_GEMV, gi, ti, s, r0, r1, dep_in[0], dep_in[1]))
+            # --- attention
+            ai = len(attns)
+            attns.append(StepAttn(self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(), self.ctx.data_ptr(),
+                                  self.ws["attn"].data_ptr(), self.tk["attn"].data_ptr(), spec.max_seq,
+                                  spec.n_heads, KVH, hd, RT.dtype_code(self.kv_dtype), self.attn_chunk,
+                                  self.nchunks, cb["odep"], 0))
+            for gg in range(KVH):
+                for c in range(self.nchunks):
+                    units.append((UNIT_ATTN, ai, gg, c, 0, 0, cb["attn"] + gg, feeds[gg]))
+            # --- o (K-split by kv group)
+            tv = _t32(t[3])
+            meta = [tile(tv, tv, 0, 0, int(ti == 0), int(ti == 0), cb["odone"], cb["odone"]) for ti in range(nt_o)]
+            go = self._group(tw["o"], tiles_tensor(meta), m=nq, n=d, nsplit=len(sp_o), x=self.ctx,
+                             prologue=C.PRO_PLAIN, ws="o", epilogue=SEPI_RESID,
+                             dbg=(T.h["attn_out"][l] if T else None, [T.bits["o"][l]] if T else None,
+                                  [K[l, 3]] if K is not None else None))
+            gi = len(groups)
+            groups.append(go)
+            for s, (r0, r1) in enumerate(sp_o):
+                for ti in range(nt_o):
+                    units.append((UNIT_GEMV, gi, ti, s, r0, r1, cb["odep"] + s, 1))
+            # --- gate/up
+            tg, tu = _t32(t[4]), _t32(t[5])
+            meta = []
+            for ti in range(nt_gu):
+                k = (ti * TH) // KC
+                meta.append(tile(tg, tu, 0, 1, int(ti == 0), int(ti == 0), cb["gu"] + k, cb["gu"] + k))
+            ggu = self._group(tw["gu"], tiles_tensor(meta), m=d, n=f, nsplit=len(sp_gu), x=self.x,
+                              gain=lw.rms_mlp, prologue=C.PRO_RMSNORM, ws="gu", epilogue=SEPI_SILU,
+                              dbg=(T.h["pre_mlp"][l] if T else None, [T.bits["gate"][l], T.bits["up"][l]] if T else None,
+                                   [K[l, 4], K[l, 5]] if K is not None else None))
+            gi = len(groups)
+            groups.append(ggu)
+            for ti in range(nt_gu):
+                for s, (r0, r1) in enumerate(sp_gu):
+                    units.append((UNIT_GEMV, gi, ti, s, r0, r1, cb["odone"], nt_o))
+            # --- down (K-chunks of whole gate/up tiles)
+            tv = _t32(t[6])
+            meta = [tile(tv, tv, 0, 0, int(ti == 0), int(ti == 0), cb["down"], cb["down"]) for ti in range(nt_dn)]
+            gdn = self._group(tw["down"], tiles_tensor(meta), m=f, n=d, nsplit=len(sp_dn), x=self.inter,
+                              prologue=C.PRO_PLAIN, ws="down", epilogue=SEPI_RESID,
+                              dbg=(T.h["mlp_inter"][l] if T else None, [T.bits["down"][l]] if T else None,
+                                   [K[l, 6]] if K is not None else None))
+            gi = len(groups)
+            groups.append(gdn)
+            for k, (r0, r1) in enumerate(sp_dn):
+                need = (r1 - 1) // TH - r0 // TH + 1
+                for ti in range(nt_dn):
+                    units.append((UNIT_GEMV, gi, ti, k, r0, r1, cb["gu"] + k, need))
+        self.lm_group = None
+        if spec.vocab:
+            nt_lm = self.lm_t.shape[0]
+            sp_lm = _splits(d, R)
+            self.ws["lm"] = torch.zeros(nt_lm * len(sp_lm) * TW, device=dev)
+            meta = [tile(float("-inf"), float("-inf"), 0, 0, 0, 0, -1, -1) for _ in range(nt_lm)]
+            glm = self._group(self.lm_t, tiles_tensor(meta), m=d, n=spec.vocab, nsplit=len(sp_lm), x=self.x,
+                              gain=self.w.final_norm, prologue=C.PRO_RMSNORM, ws="lm", epilogue=SEPI_LOGITS,
+                              y=self.logits)
+            gi = len(groups)
+            groups.append(glm)
+            last = cbase(L - 1)["down"]
+            for ti in range(nt_lm):
+                for s, (r0, r1) in enumerate(sp_lm):
+                    units.append((UNIT_GEMV, gi, ti, s, r0, r1, last, nt_dn))
+            self.cand_v = torch.zeros(nt_lm, **dict(device=dev, dtype=torch.float32))
+            self.cand_i = torch.zeros(nt_lm, device=dev, dtype=torch.int32)
+        else:
+            self.cand_v = torch.zeros(1, device=dev)
+            self.cand_i = torch.zeros(1, device=dev, dtype=torch.int32)
+        self.lm_done = torch.zeros(1, device=dev, dtype=torch.int32)
+        self._tiles = tiles_all
+        garr = (StepGroup * len(groups))(*groups)
+        self._groups = torch.frombuffer(bytearray(bytes(garr)), dtype=torch.uint8).to(dev)
+        aarr = (StepAttn * len(attns))(*attns)
+        self._attns = torch.frombuffer(bytearray(bytes(aarr)), dtype=torch.uint8).to(dev)
+        self._units = torch.tensor(units, dtype=torch.int32).to(dev)
+        self.nunits = len(units)
+        self.counters = torch.zeros(self.ncounters, device=dev, dtype=torch.int32)
+        self.ctrl = torch.zeros(4, device=dev, dtype=torch.int32)
+        p = StepPlan()
+        p.groups, p.attns, p.units = self._groups.data_ptr(), self._attns.data_ptr(), self._units.data_ptr()
+        p.counters, p.ctrl = self.counters.data_ptr(), self.ctrl.data_ptr()
+        if spec.vocab:
+            p.emb, p.emb_dtype = self.w.embedding.data_ptr(), RT.dtype_code(self.w.embedding.dtype)
+        p.x_in, p.token, p.x, p.ss, p.state = (self.x_in.data_ptr(), self.token.data_ptr(), self.x.data_ptr(),
+                                               self.ss.data_ptr(), self.state.data_ptr())
+        p.cand_v, p.cand_i, p.token_out, p.lm_done = (self.cand_v.data_ptr(), self.cand_i.data_ptr(),
+                                                      self.token.data_ptr(), self.lm_done.data_ptr())
+        p.nunits, p.ncounters, p.d = self.nunits, self.ncounters, d
+        p.w_dtype, p.ctas = RT.dtype_code(self.w_dtype), self.ctas
+        self.plan = p
+        self.unit_counts = {"total": self.nunits}
+
+    def _group(self, wt, tiles, m, n, nsplit, x, prologue, ws, epilogue, gain=None, q_out=None, k_cache=None,
+               v_cache=None, y=None, dbg=None):
+        spec = self.spec
+        g = StepGroup()
+        g.w, g.tiles, g.x = wt.data_ptr(), tiles.data_ptr(), x.data_ptr()
+        g.gain = gain.data_ptr() if gain is not None else None
+        g.ss = self.ss.data_ptr()
+        g.partials, g.tickets = self.ws[ws].data_ptr(), self.tk[ws].data_ptr()
+        g.y = y.data_ptr() if y is not None else None
+        g.resid, g.ss_out, g.inter = self.x.data_ptr(), self.ss.data_ptr(), self.inter.data_ptr()
+        g.q_out = q_out.data_ptr() if q_out is not None else None
+        g.k_cache = k_cache.data_ptr() if k_cache is not None else None
+        g.v_cache = v_cache.data_ptr() if v_cache is not None else None
+        g.rope_cos, g.rope_sin = RT.ptr(self.rope_cos), RT.ptr(self.rope_sin)
+        if dbg is not None:
+            h, bits, kept = dbg
+            g.dbg_h = RT.ptr(h) if h is not None else None
+            for i, b in enumerate(bits or []):
+                g.dbg_bits[i] = b.data_ptr()
+            for i, k in enumerate(kept or []):
+                g.kept[i] = k.data_ptr()
+        g.max_seq, g.m, g.n, g.ntiles, g.nsplit = spec.max_seq, m, n, wt.shape[0], nsplit
+        g.prologue, g.nss, g.eps, g.epilogue = prologue, spec.d_model // TW, spec.norm_eps, epilogue
+        g.nq, g.nkv, g.head_dim, g.kv_dtype = spec.n_q, spec.n_kv, spec.head_dim, RT.dtype_code(self.kv_dtype)
+        return g
+
+    # -- step -----------------------------------------------------------------
+    def reset(self, start_pos: int = 0) -> None:
+        self.state.copy_(torch.tensor([start_pos - 1, start_pos], dtype=torch.int32))
+        if start_pos == 0:
+            self.kcache.zero_()
+            self.vcache.zero_()
+
+    def launches_per_step(self) -> int:
+        return 1
+
+    def algorithmic_bytes(self, kept=None, steps: int = 1, positions: int = 0) -> float:
+        """Bytes a step must touch: kept rows x n x bw for the
+        seven projections of every layer (from `kept` [L,7] channel counts,
+        e.g. self.kept accumulated over `steps` steps), + per step m x 4
+        activation reads and n x 4 output writes per projection and the dense
+        LM head, + K and V reads of `positions` attended positions (summed
+        over the steps)."""
+        spec = self.spec
+        bw = self.tw[0]["qkv"].element_size()
+        shapes = spec.proj_shapes()
+        kept = (self.kept if kept is None else kept).double().cpu()
+        total = 0.0
+        for i, p in enumerate(PROJ):
+            n, m = shapes[p]
+            total += float(kept[:, i].sum()) * n * bw
+        steps_proj_io = sum((m * 4 + n * 4) for (n, m) in shapes.values()) * spec.n_layers
+        total += steps * steps_proj_io
+        if spec.vocab:
+            total += steps * (spec.d_model * spec.vocab * bw + spec.d_model * 4 + spec.vocab * 4)
+        kvb = torch.empty(0, dtype=self.kv_dtype).element_size()
+        total += positions * spec.n_layers * 2 * spec.n_kv * kvb
+        return total
+
+    def _launch(self, stream_h: int, from_token: bool) -> None:
+        p = self.plan
+        if from_token:
+            p.emb = self.w.embedding.data_ptr()
+        else:
+            p.emb = None
+        C.check(C.lib().teal_step_launch(ctypes.byref(p), stream_h))
+
+    def step_hidden(self, x_row) -> torch.Tensor:
+        if isinstance(x_row, torch.Tensor):
+            self.x_in.copy_(x_row.reshape(-1), non_blocking=True)
+        else:
+            self.x_in.copy_(torch.from_numpy(np.ascontiguousarray(x_row, dtype=np.float32)), non_blocking=True)
+        self._launch(RT.stream_handle(), from_token=False)
+        return self.x
+
+    def step_token(self) -> torch.Tensor:
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._launch(RT.stream_handle(), from_token=True)
+        return self.token
+
+    def step_token_host(self, tok_in: torch.Tensor, tok_out: torch.Tensor) -> None:
+        self.token.copy_(tok_in, non_blocking=True)
+        self.step_token()
+        tok_out.copy_(self.token, non_blocking=True)
+
+    def capture(self, from_token: bool = True) -> torch.cuda.CUDAGraph:
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self._launch(s.cuda_stream, from_token)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+        return g
+
+    def replay(self) -> None:
+        self.graph.replay()
