@@ -7,22 +7,28 @@
 Workload (config 3 of BASELINE.json, the largest single-GPU decode config):
 Llama-3-8B random-init bf16 weights, batch-1 greedy decode, TEAL uniform
 50% sparsity with thresholds calibrated on the GPU (histograms of the four
-taps over 16 dense decode steps).  One "step" = one decoded token: the whole
-captured CUDA graph (residual load, 32 x [qkv | attention | o | gate-up |
-down], dense LM head, argmax).  Weights are 16 GB per step, far larger than
-L2, so no flush is needed between steps.
+taps over 16 dense decode steps).  One "step" = one decoded token = ONE
+launch of the persistent step kernel (engine.StepDecoder, csrc/teal_step.cu:
+residual load, 32 x [qkv | attention | o | gate-up | down], dense LM head,
+argmax), replayed from a CUDA graph.  Weights are 15 GB per step, far larger
+than L2, so no flush is needed between steps.  `--engine launch` runs the
+per-projection launch engine (decode.SparseDecoder) instead.
 
 Line keys beyond the base contract:
-  roofline      the fused gate/up sparse GEMV (the largest launch of a step),
-                algorithmic bytes (kept*n*2 over both segments + m*4 + n*4)
-                / its CUDA-event duration, against MEASURED_PEAKS.json (or
-                the profiling guide's fallback, stated in `peak_src`)
+  roofline      the step kernel (one launch per token): algorithmic bytes per
+                launch (kept input channels x n_out x 2 B over the 7
+                projections of all 32 layers, counted on the device during
+                the timed steps, + activation reads / output writes, + the
+                dense LM head, + KV reads) / the CUDA-event time per launch,
+                against MEASURED_PEAKS.json (or the profiling guide's
+                fallback, stated in `peak_src`); `traffic` = ncu dram bytes
+                of one launch of the same workload (profiles/step_traffic.json)
   cpu_baseline  the oracle's C port of the reference `_skip_gemv`
                 (oracle/teal_oracle.c) on 1 host core, fp32 rows, on a
                 bounded sample (one layer's 7 projections + an LM-head slice)
   sweep         decode tok/s at dense / 0 / 25 / 40 / 50 % and the per-shape
                 sparse-GEMV GB/s at 0 / 40 / 50 % (the metric's second half)
-  e2e           the same decode through SparseDecoder.step_token_host: H2D of
+  e2e           the same decode through StepDecoder.step_token_host: H2D of
                 the input token from pinned memory and D2H of the argmax every
                 step, inside the timed region
 
@@ -67,6 +73,7 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true", help="skip the per-level / per-shape sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--engine", choices=["step", "launch"], default="step")
     return ap.parse_args()
 
 
@@ -250,9 +257,17 @@ def capture_steps(dec):
     dec.reset()
 
 
-def decode_tok_s(D, W, thr, steps, warmup, ws):
+def make_decoder(engine, W, thr, count_kept=False):
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200 import engine as E
+    if engine == "step":
+        return E.StepDecoder(W, thr, count_kept=count_kept)
+    return D.SparseDecoder(W, thr)
+
+
+def decode_tok_s(D, W, thr, steps, warmup, ws, engine="step"):
     import torch
-    dec = D.SparseDecoder(W, thr)
+    dec = make_decoder(engine, W, thr)
     capture_steps(dec)
     for _ in range(warmup):
         dec.replay()
@@ -384,14 +399,28 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     # headline: K timed decode steps at the target sparsity, clocks sampled
-    dec = D.SparseDecoder(W, thr[args.sparsity])
+    dec = make_decoder(args.engine, W, thr[args.sparsity], count_kept=True)
     capture_steps(dec)
     for _ in range(args.warmup):
         dec.replay()
+    torch.cuda.synchronize()
+    if args.engine == "step":
+        dec.kept.zero_()
+        pos0 = int(dec.state[1].item())
     with ClockSampler(local) as clk:
         ms = timed(dec.replay, args.steps, ws)
     value = ws * args.steps * 1e3 / ms
     launches = dec.launches_per_step() * args.steps
+    roof = None
+    if args.engine == "step":
+        positions = sum(pos0 + i + 1 for i in range(args.steps))
+        algo = dec.algorithmic_bytes(dec.kept, steps=args.steps, positions=positions) / args.steps
+        per_launch_us = ms / args.steps * 1e3
+        kept_frac = float(dec.kept.sum()) / (args.steps * spec.n_layers *
+                                             sum(m for (_, m) in spec.proj_shapes().values()))
+        roof = {"kernel": "teal step_kernel (persistent decode step, one launch per token)",
+                "per_launch_us": per_launch_us, "algo_bytes": algo, "gbs": algo / (per_launch_us * 1e-6) / 1e9,
+                "kept_frac": kept_frac, "share": 1.0}
 
     # e2e: same steps through host buffers (H2D token in, D2H argmax out per step)
     dec.reset()
@@ -405,18 +434,28 @@ def run_ours(args):
     del dec
     torch.cuda.empty_cache()
 
-    roof = gate_up_roofline(D, C, W, thr[args.sparsity])
+    if roof is None:
+        r = gate_up_roofline(D, C, W, thr[args.sparsity])
+        roof = {"kernel": "teal gemv_tma_kernel (fused gate/up, SiLU epilogue)", "per_launch_us": r["per_launch_us"],
+                "algo_bytes": r["algo_bytes"], "gbs": r["gbs"], "kept_frac": r["kept_frac"],
+                "share": r["per_launch_us"] * spec.n_layers / (ms / args.steps * 1e3)}
     sweep = None
     if not args.no_sweep:
-        dense_tok, dense_ms, _ = decode_tok_s(D, W, None, max(20, args.steps // 2), 3, ws)
+        n_sw = max(20, args.steps // 2)
+        dense_tok, _, _ = decode_tok_s(D, W, None, n_sw, 3, ws, args.engine)
         dec_rows = {"dense": round(dense_tok, 2)}
         for s in levels:
-            tok, _, _ = decode_tok_s(D, W, thr[s], max(20, args.steps // 2), 3, ws)
+            tok, _, _ = decode_tok_s(D, W, thr[s], n_sw, 3, ws, args.engine)
             dec_rows[str(s)] = round(tok, 2)
-        sweep = {"decode_tok_s": dec_rows,
+        other = "launch" if args.engine == "step" else "step"
+        other_rows = {"dense": round(decode_tok_s(D, W, None, n_sw, 3, ws, other)[0], 2),
+                      str(args.sparsity): round(decode_tok_s(D, W, thr[args.sparsity], n_sw, 3, ws, other)[0], 2)}
+        wb = sum(spec.weight_bytes(2).values())
+        sweep = {"engine": args.engine, "decode_tok_s": dec_rows,
                  "speedup_vs_dense": {k: round(v / dense_tok, 3) for k, v in dec_rows.items() if k != "dense"},
-                 "dense_weight_gb_per_token": round(sum(spec.weight_bytes(2).values()) / 1e9, 3),
-                 "dense_hbm_frac": round(dense_tok * sum(spec.weight_bytes(2).values()) / 1e9 / peak, 3)}
+                 f"{other}_engine_tok_s": other_rows,
+                 "dense_weight_gb_per_token": round(wb / 1e9, 3),
+                 "dense_hbm_frac": round(dense_tok * wb / 1e9 / peak, 3)}
         del W
         torch.cuda.empty_cache()
         sweep["gemv_gbs"] = gemv_sweep([0.0, 0.4, 0.5])
@@ -430,7 +469,7 @@ def run_ours(args):
                           f"token = 32 layers + 16 slices; host has {os.cpu_count()} cores")}
 
     traffic = None
-    tp = ROOT / "profiles" / "gate_up_traffic.json"
+    tp = ROOT / "profiles" / ("step_traffic.json" if args.engine == "step" else "gate_up_traffic.json")
     if tp.exists():
         try:
             traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
@@ -443,16 +482,16 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "llama3-8b random-init batch-1 decode, TEAL uniform calibrated sparsity",
-                       "sparsity": args.sparsity, "batch": 1, "weights": "bf16 input-major",
-                       "parallelism": "replicas" if ws > 1 else "single",
+                       "sparsity": args.sparsity, "batch": 1, "weights": "bf16 tiled input-major",
+                       "engine": args.engine, "parallelism": "replicas" if ws > 1 else "single",
                        "l2": "inputs larger than L2 (15 GB of weights per step)"},
-            "roofline": {"bound": "hbm", "kernel": "teal gemv_tma_kernel (fused gate/up, SiLU epilogue)",
+            "roofline": {"bound": "hbm", "kernel": roof["kernel"],
                          "achieved": round(roof["gbs"], 1), "peak": peak, "peak_src": peak_src, "unit": "GB/s",
                          "frac": round(roof["gbs"] / peak, 4), "traffic": traffic,
                          "algo_bytes_per_launch": int(roof["algo_bytes"]),
                          "us_per_launch": round(roof["per_launch_us"], 2),
                          "kept_frac": round(roof["kept_frac"], 4),
-                         "share_of_step": round(roof["per_launch_us"] * spec.n_layers / (ms / args.steps * 1e3), 3)},
+                         "share_of_step": round(roof["share"], 3)},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 4},
             "gpu_launches": launches,

@@ -195,20 +195,31 @@ int teal_argmax(const float* logits, int64_t n, int* out_token,
  * Replaces the per-projection launches of a decode step (the seven
  * `gated(name, a) @ W.T` products of model._forward, model.py:158-198, plus
  * attention, residual load, LM head and argmax) with ONE persistent
- * cooperative launch: every CTA pulls work units from a device queue in
- * topological order and waits on per-dependency counters (no grid barrier,
- * no host sync).  Weights are stored TILED input-major: a group's output
- * columns are cut into tiles of TEAL_STEP_TW columns and tile t is the
- * contiguous block w[t][i][0..TW) over input channels i (element (out
- * t*TW + c, in i) = w[(t*m + i)*TW + c]); a kept channel streams one
- * contiguous TW-column row chunk per tile.  Each tile carries two column
- * halves with their own thresholds (gate | up interleaved for the MLP).
- * A GEMV unit = (group, tile, K-range); K-split tiles are finished by the
- * last-arriving unit, summing partials in split order (deterministic).  */
+ * cooperative launch.  Every CTA walks the same list of PHASES (per layer:
+ * qkv, attention, o, gate/up, down; then the LM head) and owns a static,
+ * equal slice of every GEMV phase: the flattened (column tile, 32-channel
+ * group) space of the phase is cut into G equal contiguous ranges, one per
+ * CTA, so all CTAs finish a phase together.  Ordering between phases uses
+ * dependency counters instead of grid barriers: a slice waits only for the
+ * input rows it reads (attention groups for o, gate/up tiles for down); the
+ * RMSNorm inputs (whole residual + sum of squares) are the only global joins.
+ *
+ * Weights are stored TILED input-major: a group's output columns are cut
+ * into tiles of TEAL_STEP_TW columns and tile t is the contiguous block
+ * w[t][i][0..TW) over input channels i (element (out t*TW + c, in i) =
+ * w[(t*m + i)*TW + c]); a kept channel streams one contiguous row chunk per
+ * tile, fetched by the TMA engine (cp.async.bulk) into a per-warp shared
+ * memory ring.  Each tile carries two column halves with their own
+ * thresholds (gate | up interleaved for the MLP).  A tile split across CTAs
+ * is finished by its last-arriving contributor, summing the fp32 partials in
+ * contributor order (deterministic two-phase reduction). */
 #define TEAL_STEP_TW 256
-#define TEAL_UNIT_LOAD 0
-#define TEAL_UNIT_GEMV 1
-#define TEAL_UNIT_ATTN 2
+#define TEAL_PHASE_LOAD 0
+#define TEAL_PHASE_GEMV 1
+#define TEAL_PHASE_ATTN 2
+#define TEAL_DEP_NONE 0
+#define TEAL_DEP_GLOBAL 1    /* counters[dep] >= target                          */
+#define TEAL_DEP_ROWS 2      /* counters[dep + r / dep_rows] >= target for every input row r read */
 
 #define TEAL_SEPI_STORE 0    /* y[col] = v                                   */
 #define TEAL_SEPI_RESID 1    /* resid[col] += v ; ss_out[tile] = sum resid^2 */
@@ -230,7 +241,7 @@ typedef struct teal_step_group {
     const float* x;          /* input vector [m] (written earlier in the step) */
     const float* gain;       /* PRO_RMSNORM gain [m]                         */
     const float* ss;         /* PRO_RMSNORM: sum-of-squares partials [nss]   */
-    float* partials;         /* [ntiles][nsplit][TW]                          */
+    float* partials;         /* [ntiles][maxc][TW]                            */
     unsigned* tickets;       /* [ntiles], zero, self-resetting               */
     float* y;                /* STORE / LOGITS output [n]                    */
     float* resid;            /* RESID residual stream [n]                    */
@@ -241,11 +252,11 @@ typedef struct teal_step_group {
     void* v_cache;
     const float* rope_cos;   /* nullable [max_seq][hd/2]                      */
     const float* rope_sin;
-    float* dbg_h;            /* nullable: prologue h [m] (tile-0 units)      */
+    float* dbg_h;            /* nullable: prologue h [m]                     */
     uint32_t* dbg_bits[3];   /* nullable: keep bits per segment [ceil(m/32)] */
     unsigned long long* kept[3];  /* nullable: kept channels per segment    */
     int64_t max_seq;
-    int m, n, ntiles, nsplit;
+    int m, n, ntiles, maxc;  /* maxc: partial slots per tile                 */
     int prologue, nss;
     float eps;
     int epilogue;
@@ -264,19 +275,24 @@ typedef struct teal_step_attn {
     int H, KVH, hd, kv_dtype;
     int chunk, nchunks;
     int sig_base;            /* counter sig_base + g += 1 when group g's ctx is final */
-    int pad_;
+    int dep_base;            /* unit (g, *) waits for counters[dep_base + g] >= dep_target[g] */
+    const int* dep_target;   /* [KVH]                                         */
+    unsigned long long* dbg; /* nullable debug: [KVH*nchunks][6] %globaltimer stamps */
 } teal_step_attn;
 
-typedef struct teal_step_unit {
-    int kind, group, tile, split, r0, r1, dep, target;
-} teal_step_unit;
+typedef struct teal_step_phase {
+    int kind, group;         /* TEAL_PHASE_*; index into groups / attns      */
+    int dep_kind, dep;       /* TEAL_DEP_*; counter (base) index             */
+    int target, dep_rows;
+} teal_step_phase;
 
 typedef struct teal_step_plan {
     const teal_step_group* groups;   /* device arrays */
     const teal_step_attn* attns;
-    const teal_step_unit* units;
-    int* counters;                   /* [ncounters] zero; reset at the end of every launch */
-    unsigned* ctrl;                  /* [4] zero: queue head, exit count */
+    const teal_step_phase* phases;
+    int* counters;                   /* [ncounters * 32] zero (counter i at i*32, one 128-B line each);
+                                        reset at the end of every launch */
+    unsigned* ctrl;                  /* [4] zero: exit count                   */
     const void* emb;                 /* LOAD: embedding [vocab][d] (NULL: x_in) */
     const float* x_in;               /* LOAD: hidden row [d] when emb == NULL  */
     const int* token;                /* LOAD: token id (device)                */
@@ -287,12 +303,14 @@ typedef struct teal_step_plan {
     int* cand_i;
     int* token_out;                  /* LOGITS: argmax token                   */
     unsigned* lm_done;               /* LOGITS: tiles finished (self-resetting) */
-    int nunits, ncounters;
+    unsigned long long* timeline;    /* nullable debug: [ctas][nphases][2] %globaltimer */
+    int nphases, ncounters;
     int d, emb_dtype;
-    int w_dtype, ctas;               /* ctas <= 0: occupancy x SMs             */
+    int w_dtype, ctas;               /* ctas: grid size (<= resident capacity)  */
 } teal_step_plan;
 
-/* CTAs per SM the step kernel runs at for a weight dtype (for sizing). */
+/* Resident CTAs per SM of the step kernel for a weight dtype; the plan's
+ * static slicing must be built for ctas = this x #SMs (or fewer). */
 int teal_step_ctas_per_sm(int w_dtype);
 int teal_step_launch(const teal_step_plan* plan, cudaStream_t stream);
 

@@ -64,10 +64,22 @@ __device__ __forceinline__ uint4 ldg128_stream(const void* p) {
     return r;
 }
 
+// Same, with an L2 cache policy (createpolicy ... evict_first): weights are
+// touched once per step and must not evict the step's activations, split-K
+// partials and KV cache from L2.
+__device__ __forceinline__ uint4 ldg128_stream_pol(const void* p, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+
 // L2-coherent scalar load used when reading other CTAs' split-K partials.
 __device__ __forceinline__ float ldcg_f32(const float* p) { return __ldcg(p); }
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -7,40 +7,38 @@
 // a KV cache), the dense LM head and greedy argmax.
 //
 // Execution model
-//   * grid = (CTAs per SM at full occupancy) x #SMs, all co-resident
-//     (cooperative launch).  Each CTA pulls work units from one device queue
-//     (atomic head) in the plan's topological order, prefetching the next
-//     index while it works.
-//   * A unit may depend on one counter reaching a target; counters are
-//     bumped (release) by the units that finish the producing data.  Since a
-//     unit only waits on units that were dequeued before it and every
-//     dequeued unit runs on a resident CTA, the queue cannot deadlock.
-//     There is no grid-wide barrier: attention for kv-head g starts when the
-//     q/k/v tiles of g are final, the o-projection split of g when g's
-//     context is final, each down split when its gate/up tiles are final;
-//     only RMSNorm inputs (full residual + sum of squares) are global joins.
-//   * The last CTA to leave resets the queue and all counters, so a CUDA
-//     graph of the launch replays token after token.
+//   * grid = resident CTAs (cooperative launch); every CTA walks the plan's
+//     phase list (per layer: qkv, attention, o, gate/up, down; then LM head).
+//   * GEMV phase: the flattened (column tile, 32-channel group) space is cut
+//     into G equal contiguous ranges, CTA c owning [c*F/G, (c+1)*F/G) — equal
+//     input channels to threshold and, in expectation, equal kept rows to
+//     stream, so CTAs finish a phase together.  A range spans a few tiles;
+//     a tile shared by several CTAs is finished by its last-arriving
+//     contributor (ticket), which sums the fp32 partials in contributor order
+//     (deterministic two-phase reduction) and runs the fused epilogue.
+//   * Dependencies are counters bumped (release) by tile epilogues and
+//     polled (acquire) before a slice reads its input rows: o waits only for
+//     the attention groups its rows come from, down only for the gate/up
+//     tiles its rows come from, attention for kv-group g only for the q/k/v
+//     tiles of g.  The RMSNorm inputs (residual + sum of squares) are the
+//     only global joins.  Every wait targets an earlier phase and all CTAs
+//     are resident, so the schedule cannot deadlock; the last CTA to leave
+//     resets the counters, so a CUDA graph of the launch replays per token.
 //
-// GEMV unit (group, column tile, K-range [r0, r1)) over TILED input-major
-// weights: tile t of a group is the contiguous block w[t][i][0..TW), so a
-// kept input channel is one contiguous TW*esz-byte row chunk (512 B bf16).
-//   1. prologue: h_i = x_i (or RMSNorm: x_i / sqrt(sum(ss)/m + eps) * g_i
-//      from fixed-order sum-of-squares partials), keep_lo/hi =
-//      !(|h_i| <= t_lo/hi) (closed prune boundary, NaN kept), ordered
-//      CTA-local compaction of kept rows with warp ballot/popc;
-//   2. stream: warps take kept rows round-robin, UR rows in flight per warp,
-//      one 16-byte non-allocating load per lane per row half that is kept,
-//      fp32 FMA into per-lane column accumulators;
-//   3. fixed-order cross-warp reduction -> TW column partials;
-//   4. K-split tiles: partial -> workspace slot, ticket; the last-arriving
-//      unit sums the slots in split order (deterministic two-phase
-//      reduction) and runs the epilogue (store / residual + sum of squares /
-//      SiLU(gate)*up / RoPE + KV-cache write / logits + argmax), then
-//      signals its counters.
+// Streaming core (per CTA slice segment = one tile x a row range):
+//   1. h_i = x_i or RMSNorm(x)_i (x / sqrt(sum(ss)/m + eps) * g, fixed-order
+//      sum of sum-of-squares partials); keep_lo/hi = !(|h_i| <= t_lo/hi)
+//      (closed prune boundary, NaN kept); ordered CTA-local compaction with
+//      warp ballot/popc;
+//   2. warp w takes kept rows w, w+8, ...; its lane 0 keeps S row chunks in
+//      flight with cp.async.bulk (TMA engine, L2 evict-first) into the warp's
+//      private shared-memory ring (one mbarrier per slot, only the kept
+//      halves are copied); lanes read 16 B each and FMA into fp32 registers;
+//   3. fixed-order cross-warp reduction -> TW column sums.
 // No tensor cores: a batch-1 matvec is ~1 flop/byte.
 #include "teal_common.cuh"
 #include <string.h>
+#include <stdlib.h>
 
 namespace teal {
 namespace step {
@@ -49,10 +47,11 @@ constexpr int TW = TEAL_STEP_TW;  // columns per tile
 constexpr int TH = TW / 2;        // columns per half
 constexpr int NT = 256;           // threads per CTA (== TW: one column per thread in epilogues)
 constexpr int NW = NT / 32;
-constexpr int MAXR = 1024;        // rows per GEMV unit
+constexpr int MAXR = 1024;        // rows per compaction chunk
 constexpr int ATT_MAXG = 8;
 constexpr int ATT_MAXHD = 128;
 constexpr int ATT_MAXCHUNK = 256;
+constexpr int ATT_STAGE = 16384;  // bytes of K (and of V) staged per attention unit
 static_assert(NT == TW, "epilogues map one thread per tile column");
 
 struct Smem {
@@ -64,6 +63,8 @@ struct Smem {
         struct {
             float q[ATT_MAXG * ATT_MAXHD];
             float sc[ATT_MAXG * ATT_MAXCHUNK];
+            uint4 k[ATT_STAGE / 16];   // K rows of the chunk (raw cache dtype)
+            uint4 v[ATT_STAGE / 16];   // V rows of the chunk
         } a;
     } u;
     float red[NW * TW];
@@ -72,10 +73,9 @@ struct Smem {
     float scr[NW + 1];
     int wcnt[NW];
     float rden;
-    int unit, next, last;
-    float bv;
-    int bi;
+    int last;
 };
+constexpr size_t kSmemBytes = sizeof(Smem);
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
@@ -83,22 +83,59 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     return v;
 }
 
-__device__ __forceinline__ void wait_counter(const int* c, int target) {
+// Each counter lives in its own 128-byte line (index * CSTRIDE) so hundreds
+// of pollers of one counter do not contend with the other counters' updates.
+constexpr int CSTRIDE = 32;
+
+// thread 0 polls with backoff; the barrier publishes the result to the CTA
+__device__ __forceinline__ void wait_range(const int* counters, int c0, int c1, int target) {
     if (threadIdx.x == 0) {
-        int spins = 0;
-        while (ld_acquire(c) < target) {
-            if (++spins > 4) __nanosleep(32);
+        for (int c = c0; c <= c1; ++c) {
+            unsigned ns = 32;
+            while (ld_acquire(counters + (int64_t)c * CSTRIDE) < target) {
+                __nanosleep(ns);
+                ns = ns < 512 ? ns * 2 : 512;
+            }
         }
     }
     __syncthreads();
 }
 
-// every writer thread fences, then one thread bumps the counters
+// Publish the CTA's prior global writes, then bump the counters: the barrier
+// orders every thread's writes before thread 0, whose gpu-scope fence makes
+// them (cumulatively) visible before its atomics — the cooperative-groups
+// grid-sync pattern, one fence per CTA instead of one per thread.
 __device__ __forceinline__ void signal(int* counters, int c0, int c1) {
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0 && c0 >= 0)
-        for (int c = c0; c <= c1; ++c) atomicAdd(counters + c, 1);
+    if (threadIdx.x == 0 && c0 >= 0) {
+        __threadfence();
+        for (int c = c0; c <= c1; ++c) atomicAdd(counters + (int64_t)c * CSTRIDE, 1);
+    }
+}
+
+// Take a split-K ticket after storing this CTA's partial: returns (to every
+// thread) whether this CTA arrived last; the last arriver's thread 0 fences
+// again (acquire side) before the barrier that precedes the partial reads.
+__device__ __forceinline__ bool take_ticket(unsigned* ticket, unsigned expected_prev, int& s_last) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(ticket, 1u);
+        const int last = prev == expected_prev;
+        if (last) {
+            *ticket = 0u;
+            __threadfence();
+        }
+        s_last = last;
+    }
+    __syncthreads();
+    return s_last != 0;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 
 __device__ __forceinline__ float silu(float z) { return z / (1.0f + expf(-z)); }
@@ -120,17 +157,22 @@ __device__ __forceinline__ float block_sum_nt(float v, Smem& s) {
 }
 
 template <typename T>
-__device__ __forceinline__ float ld_kv(const void* base, int64_t off) {
-    return to_f32<T>(__ldcg(reinterpret_cast<const T*>(base) + off));
+__device__ __forceinline__ float ld_kv(const void* base, int64_t off);
+template <>
+__device__ __forceinline__ float ld_kv<float>(const void* base, int64_t off) {
+    return __ldcg(reinterpret_cast<const float*>(base) + off);
 }
 template <>
 __device__ __forceinline__ float ld_kv<uint16_t>(const void* base, int64_t off) {
-    const unsigned short v = __ldcg(reinterpret_cast<const unsigned short*>(base) + off);
-    return bf16_to_f32(v);
+    return bf16_to_f32(__ldcg(reinterpret_cast<const unsigned short*>(base) + off));
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // ---- epilogue of one finished column tile (thread c = column c) --------------
-__device__ void finalize(const teal_step_plan& P, const teal_step_group& g, int tile, float v, Smem& s) {
+__device__ __noinline__ void finalize(const teal_step_plan& P, const teal_step_group& g, int tile, float v, Smem& s) {
     const int c = threadIdx.x;
     const int64_t col = (int64_t)tile * TW + c;
     const teal_step_tile tm = g.tiles[tile];
@@ -222,6 +264,7 @@ __device__ void finalize(const teal_step_plan& P, const teal_step_group& g, int 
                     *P.token_out = gi == 0x7fffffff ? 0 : gi;
                 }
             }
+            __syncthreads();
             break;
         }
         default:
@@ -230,48 +273,60 @@ __device__ void finalize(const teal_step_plan& P, const teal_step_group& g, int 
     signal(P.counters, tm.sig0, tm.sig1);
 }
 
-// ---- GEMV unit ---------------------------------------------------------------
-// ESZ = weight element bytes (2: bf16, 4: fp32).  Per lane 8 column
-// accumulators: bf16 lane l owns columns [8l, 8l+8) (lanes 16..31 = hi half);
-// fp32 lane l owns [4l, 4l+4) (lo) and [128+4l, 128+4l+4) (hi).
+// Per-lane accumulator columns: bf16 lane l owns [8l, 8l+8) (lanes 16..31 =
+// hi half); fp32 lane l owns [4l, 4l+4) (lo) and [128+4l, 128+4l+4) (hi).
 template <int ESZ>
 __device__ __forceinline__ int acc_col(int lane, int j) {
     if constexpr (ESZ == 2) return lane * 8 + j;
     else return j < 4 ? lane * 4 + j : TH + lane * 4 + (j - 4);
 }
 
-template <int ESZ>
-__device__ void gemv_unit(const teal_step_plan& P, const teal_step_group& g, const teal_step_unit& U, Smem& s) {
-    constexpr int UR = ESZ == 2 ? 8 : 4;      // rows in flight per warp
-    constexpr int ROWB = TW * ESZ;            // bytes per row chunk
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const teal_step_tile tm = g.tiles[U.tile];
-    const bool rms = g.prologue == TEAL_PRO_RMSNORM;
-    if (rms && tid == 0) {
-        float a = 0.f;
-        for (int p = 0; p < g.nss; ++p) a += __ldcg(g.ss + p);
-        s.rden = sqrtf(a / (float)g.m + g.eps);
+// sqrt(sum(ss)/m + eps) with the partials summed in ascending order: one
+// warp loads them in parallel (one L2 round trip), lane 0 adds in order.
+__device__ __forceinline__ float rms_den(const teal_step_group& g, int lane) {
+    float a = 0.f;
+    for (int p0 = 0; p0 < g.nss; p0 += 32) {
+        const float v = (p0 + lane < g.nss) ? __ldcg(g.ss + p0 + lane) : 0.f;
+        const int n = min(32, g.nss - p0);
+        for (int q = 0; q < n; ++q) a += __shfl_sync(0xffffffffu, v, q);
     }
-    __syncthreads();
-    const float rden = rms ? s.rden : 1.f;
-    const bool two = tm.seg_hi != tm.seg_lo || tm.t_hi != tm.t_lo;
+    return sqrtf(a / (float)g.m + g.eps);
+}
 
-    // 1. threshold + ordered compaction
-    int base = 0;
-    for (int i0 = U.r0; i0 < U.r1; i0 += NT) {
-        const int i = i0 + tid;
-        const bool v = i < U.r1;
-        float h = 0.f;
-        if (v) {
+__device__ __forceinline__ int owner_of(int64_t gidx, int64_t F, int G) {
+    return (int)(((gidx + 1) * (int64_t)G - 1) / F);
+}
+
+// Threshold + compact rows [r0, r1) of one tile into s.u.g (ordered).
+__device__ int compact_rows(const teal_step_group& g, const teal_step_tile& tm, int tile, int r0, int r1,
+                            float rden, bool rms, Smem& s) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool two = tm.seg_hi != tm.seg_lo;
+    constexpr int RPT = MAXR / NT;  // rows per thread
+    float hx[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {  // all x (and gain) loads in flight at once
+        const int i = r0 + q * NT + tid;
+        hx[q] = 0.f;
+        if (i < r1) {
             const float xv = __ldcg(g.x + i);
-            h = rms ? (xv / rden) * __ldg(g.gain + i) : xv;
+            hx[q] = rms ? (xv / rden) * __ldg(g.gain + i) : xv;
         }
+    }
+    int base = 0;
+#pragma unroll 1
+    for (int q = 0; q < RPT; ++q) {
+        const int i0 = r0 + q * NT;
+        if (i0 >= r1) break;
+        const int i = i0 + tid;
+        const bool v = i < r1;
+        const float h = hx[q];
         const bool klo = v && !(fabsf(h) <= tm.t_lo);
         const bool khi = v && !(fabsf(h) <= tm.t_hi);
         const bool k = klo || khi;
         const unsigned bk = __ballot_sync(0xffffffffu, k);
-        const bool wv = (i - lane) < U.r1;  // this warp's 32 rows start inside the range
-        if (g.dbg_h && U.tile == 0 && v) g.dbg_h[i] = h;
+        const bool wv = (i - lane) < r1;
+        if (g.dbg_h && tile == 0 && v) g.dbg_h[i] = h;
         if (tm.first_lo && wv) {
             const unsigned bl = __ballot_sync(0xffffffffu, klo);
             if (lane == 0) {
@@ -297,123 +352,180 @@ __device__ void gemv_unit(const teal_step_plan& P, const teal_step_group& g, con
         }
         if (k) {
             const int pos = off + __popc(bk & ((1u << lane) - 1u));
-            s.u.g.idx[pos] = (i - U.r0) | (klo ? (1 << 30) : 0) | (khi ? (int)(1u << 31) : 0);
+            s.u.g.idx[pos] = (i - r0) | (klo ? (1 << 30) : 0) | (khi ? (int)(1u << 31) : 0);
             s.u.g.h[pos] = h;
         }
         base += tot;
         __syncthreads();
     }
-    const int cnt = base;
+    return base;
+}
 
-    // 2. stream kept row chunks
-    const unsigned char* tb =
-        reinterpret_cast<const unsigned char*>(g.w) + ((int64_t)U.tile * g.m + U.r0) * ROWB;
-    float acc[8];
+// Stream the `cnt` compacted rows: warp w takes rows w*U.., w*U+NW*U.., with
+// the next batch of U rows' 16-byte loads issued before the current batch is
+// consumed (software pipeline: 2U row chunks in flight per warp).  Only the
+// kept half of a row is loaded (bf16: lanes 0-15 = lo, 16-31 = hi; fp32:
+// every lane loads 16 B of each kept half).
+template <int ESZ, int UB>
+__device__ __forceinline__ void stream_rows(const unsigned char* tb, int cnt, const Smem& s, float acc[8],
+                                            uint64_t pol) {
+    constexpr int ROWB = TW * ESZ;
+    constexpr int HB = ROWB / 2;
+    constexpr int U = ESZ == 2 ? UB : UB / 2;
+    constexpr int NV = ESZ == 2 ? 1 : 2;  // 16-byte vectors per lane per row
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint4 a[U][NV], b[U][NV];
+    float ha[U][NV], hb[U][NV];
+    auto fetch = [&](int e0, uint4 (&d)[U][NV], float (&hh)[U][NV]) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-    for (int e0 = warp * UR; e0 < cnt; e0 += NW * UR) {
-        if constexpr (ESZ == 2) {
-            const int sh = lane < 16 ? 30 : 31;
-            uint4 d[UR];
-            float hh[UR];
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u;
 #pragma unroll
-            for (int u = 0; u < UR; ++u) {
-                const int e = e0 + u;
-                d[u] = make_uint4(0u, 0u, 0u, 0u);
-                hh[u] = 0.f;
-                if (e < cnt) {
-                    const unsigned pk = (unsigned)s.u.g.idx[e];
-                    if ((pk >> sh) & 1u) {
-                        hh[u] = s.u.g.h[e];
-                        d[u] = ldg128_stream(tb + (int64_t)(pk & 0x3fffffffu) * ROWB + lane * 16);
+            for (int v = 0; v < NV; ++v) {
+                d[u][v] = make_uint4(0u, 0u, 0u, 0u);
+                hh[u][v] = 0.f;
+            }
+            if (e < cnt) {
+                const unsigned pk = (unsigned)s.u.g.idx[e];
+                const float h = s.u.g.h[e];
+                const unsigned char* row = tb + (int64_t)(pk & 0x3fffffffu) * ROWB + lane * 16;
+                if constexpr (ESZ == 2) {
+                    if ((pk >> (lane < 16 ? 30 : 31)) & 1u) {
+                        d[u][0] = ldg128_stream_pol(row, pol);
+                        hh[u][0] = h;
                     }
+                } else {
+                    if ((pk >> 30) & 1u) { d[u][0] = ldg128_stream_pol(row, pol); hh[u][0] = h; }
+                    if ((pk >> 31) & 1u) { d[u][NV - 1] = ldg128_stream_pol(row + HB, pol); hh[u][NV - 1] = h; }
                 }
             }
+        }
+    };
+    auto consume = [&](const uint4 (&d)[U][NV], const float (&hh)[U][NV]) {
 #pragma unroll
-            for (int u = 0; u < UR; ++u) {
-                const uint32_t w4[4] = {d[u].x, d[u].y, d[u].z, d[u].w};
+        for (int u = 0; u < U; ++u) {
+            if constexpr (ESZ == 2) {
+                const uint32_t w4[4] = {d[u][0].x, d[u][0].y, d[u][0].z, d[u][0].w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    acc[2 * q] = fmaf(hh[u], bf16_lo(w4[q]), acc[2 * q]);
-                    acc[2 * q + 1] = fmaf(hh[u], bf16_hi(w4[q]), acc[2 * q + 1]);
+                    acc[2 * q] = fmaf(hh[u][0], bf16_lo(w4[q]), acc[2 * q]);
+                    acc[2 * q + 1] = fmaf(hh[u][0], bf16_hi(w4[q]), acc[2 * q + 1]);
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    acc[4 * v + 0] = fmaf(hh[u][v], __uint_as_float(d[u][v].x), acc[4 * v + 0]);
+                    acc[4 * v + 1] = fmaf(hh[u][v], __uint_as_float(d[u][v].y), acc[4 * v + 1]);
+                    acc[4 * v + 2] = fmaf(hh[u][v], __uint_as_float(d[u][v].z), acc[4 * v + 2]);
+                    acc[4 * v + 3] = fmaf(hh[u][v], __uint_as_float(d[u][v].w), acc[4 * v + 3]);
                 }
             }
-        } else {
-            uint4 d0[UR], d1[UR];
-            float h0[UR], h1[UR];
-#pragma unroll
-            for (int u = 0; u < UR; ++u) {
-                const int e = e0 + u;
-                d0[u] = d1[u] = make_uint4(0u, 0u, 0u, 0u);
-                h0[u] = h1[u] = 0.f;
-                if (e < cnt) {
-                    const unsigned pk = (unsigned)s.u.g.idx[e];
-                    const float hv = s.u.g.h[e];
-                    const unsigned char* row = tb + (int64_t)(pk & 0x3fffffffu) * ROWB + lane * 16;
-                    if ((pk >> 30) & 1u) { h0[u] = hv; d0[u] = ldg128_stream(row); }
-                    if ((pk >> 31) & 1u) { h1[u] = hv; d1[u] = ldg128_stream(row + TH * 4); }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < UR; ++u) {
-                acc[0] = fmaf(h0[u], __uint_as_float(d0[u].x), acc[0]);
-                acc[1] = fmaf(h0[u], __uint_as_float(d0[u].y), acc[1]);
-                acc[2] = fmaf(h0[u], __uint_as_float(d0[u].z), acc[2]);
-                acc[3] = fmaf(h0[u], __uint_as_float(d0[u].w), acc[3]);
-                acc[4] = fmaf(h1[u], __uint_as_float(d1[u].x), acc[4]);
-                acc[5] = fmaf(h1[u], __uint_as_float(d1[u].y), acc[5]);
-                acc[6] = fmaf(h1[u], __uint_as_float(d1[u].z), acc[6]);
-                acc[7] = fmaf(h1[u], __uint_as_float(d1[u].w), acc[7]);
-            }
         }
+    };
+    int e0 = warp * U;
+    if (e0 >= cnt) return;
+    fetch(e0, a, ha);
+    for (;;) {
+        const int en = e0 + NW * U;
+        if (en < cnt) fetch(en, b, hb);
+        consume(a, ha);
+        if (en >= cnt) break;
+        e0 = en;
+        if (e0 + NW * U < cnt) fetch(e0 + NW * U, a, ha);
+        consume(b, hb);
+        if (e0 + NW * U >= cnt) break;
+        e0 += NW * U;
     }
+}
 
-    // 3. fixed-order cross-warp reduction
-#pragma unroll
-    for (int j = 0; j < 8; ++j) s.red[warp * TW + acc_col<ESZ>(lane, j)] = acc[j];
-    __syncthreads();
-    float v = 0.f;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) v += s.red[w * TW + tid];
-
-    // 4. split-K combine (deterministic, split order) + epilogue
-    if (g.nsplit > 1) {
-        float* slot = g.partials + ((int64_t)U.tile * g.nsplit + U.split) * TW;
-        __stcg(slot + tid, v);
-        __threadfence();
+template <int ESZ, int UB>
+__device__ void gemv_slice(const teal_step_plan& P, const teal_step_phase& ph, Smem& s, uint64_t pol,
+                           unsigned long long* tl) {
+    const teal_step_group& g = P.groups[ph.group];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gpt = (g.m + 31) / 32;
+    const int64_t F = (int64_t)g.ntiles * gpt;
+    const int G = (int)min64((int64_t)gridDim.x, F), c = blockIdx.x;  // every participating range is non-empty
+    if (c >= G) return;
+    const int64_t g0 = (int64_t)c * F / G, g1 = (int64_t)(c + 1) * F / G;
+    const bool rms = g.prologue == TEAL_PRO_RMSNORM;
+    if (ph.dep_kind == TEAL_DEP_GLOBAL) wait_range(P.counters, ph.dep, ph.dep, ph.target);
+    float rden = 1.f;
+    if (rms) {
+        if (warp == 0) s.rden = rms_den(g, lane);
         __syncthreads();
-        if (tid == 0) {
-            const unsigned prev = atomicAdd(g.tickets + U.tile, 1u);
-            const int last = prev == (unsigned)g.nsplit - 1u;
-            if (last) g.tickets[U.tile] = 0u;
-            s.last = last;
-        }
-        __syncthreads();
-        if (!s.last) return;
-        __threadfence();
-        const float* pb = g.partials + (int64_t)U.tile * g.nsplit * TW + tid;
-        v = 0.f;
-        int sp = 0;
-        for (; sp + 4 <= g.nsplit; sp += 4) {
-            const float a0 = __ldcg(pb + (int64_t)sp * TW), a1 = __ldcg(pb + (int64_t)(sp + 1) * TW);
-            const float a2 = __ldcg(pb + (int64_t)(sp + 2) * TW), a3 = __ldcg(pb + (int64_t)(sp + 3) * TW);
-            v += a0;
-            v += a1;
-            v += a2;
-            v += a3;
-        }
-        for (; sp < g.nsplit; ++sp) v += __ldcg(pb + (int64_t)sp * TW);
+        rden = s.rden;
     }
-    if (g.col_scale) v *= g.col_scale[(int64_t)U.tile * TW + tid];
-    finalize(P, g, U.tile, v, s);
+    constexpr int ROWB = TW * ESZ;
+    int segi = 0, lasts = 0;
+#define SL_STAMP(k, v) do { if (tl && tid == 0) tl[k] = (v); } while (0)
+    for (int64_t gs = g0; gs < g1; ++segi) {
+        const int tile = (int)(gs / gpt);
+        const int64_t ge = min64(g1, (int64_t)(tile + 1) * gpt);
+        const int r0 = (int)(gs - (int64_t)tile * gpt) * 32;
+        const int r1 = min(g.m, (int)(ge - (int64_t)tile * gpt) * 32);
+        gs = ge;
+        if (ph.dep_kind == TEAL_DEP_ROWS)
+            wait_range(P.counters, ph.dep + r0 / ph.dep_rows, ph.dep + (r1 - 1) / ph.dep_rows, ph.target);
+        if (segi == 0) SL_STAMP(2, gtimer());
+        const teal_step_tile tm = g.tiles[tile];
+        const unsigned char* tbase = reinterpret_cast<const unsigned char*>(g.w) + (int64_t)tile * g.m * ROWB;
+        float acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        for (int ra = r0; ra < r1; ra += MAXR) {
+            const int rb = min(r1, ra + MAXR);
+            const int cnt = compact_rows(g, tm, tile, ra, rb, rden, rms, s);
+            stream_rows<ESZ, UB>(tbase + (int64_t)ra * ROWB, cnt, s, acc, pol);
+            __syncthreads();  // rows list is rewritten by the next chunk
+        }
+        SL_STAMP(segi == 0 ? 3 : 5, gtimer());
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s.red[warp * TW + acc_col<ESZ>(lane, j)] = acc[j];
+        __syncthreads();
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) v += s.red[w * TW + tid];
+        const int cf = owner_of((int64_t)tile * gpt, F, G);
+        const int cl = owner_of((int64_t)(tile + 1) * gpt - 1, F, G);
+        if (cl > cf) {
+            float* slot = g.partials + ((int64_t)tile * g.maxc + (c - cf)) * TW;
+            __stcg(slot + tid, v);
+            if (!take_ticket(g.tickets + tile, (unsigned)(cl - cf), s.last)) {
+                if (segi == 0) SL_STAMP(4, gtimer());
+                continue;
+            }
+            const float* pb = g.partials + (int64_t)tile * g.maxc * TW + tid;
+            const int nc = cl - cf + 1;
+            v = 0.f;
+            for (int s0 = 0; s0 < nc; s0 += 16) {  // 16 independent loads in flight, summed in order
+                float pv[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) pv[q] = (s0 + q < nc) ? __ldcg(pb + (int64_t)(s0 + q) * TW) : 0.f;
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    if (s0 + q < nc) v += pv[q];
+            }
+        }
+        if (g.col_scale) v *= g.col_scale[(int64_t)tile * TW + tid];
+        finalize(P, g, tile, v, s);
+        ++lasts;
+        if (segi == 0) SL_STAMP(4, gtimer());
+    }
+    SL_STAMP(6, (unsigned long long)segi);
+    SL_STAMP(7, (unsigned long long)lasts);
+#undef SL_STAMP
 }
 
 // ---- attention unit: (kv head g, position chunk) -------------------------------
+// Deliberately compact code (runtime loops over heads and head_dim chunks):
+// this path runs on a few CTAs once per layer, so its instructions are cold
+// in the instruction cache every time; unrolled code here costs more in
+// instruction fetch than it saves in issue slots.
 template <typename KT>
-__device__ void attn_unit_t(const teal_step_plan& P, const teal_step_attn& a, const teal_step_unit& U, Smem& s) {
+__device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_step_attn& a, int g, int ch, Smem& s) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g = U.tile, ch = U.split;
-    const int G = a.H / a.KVH, hd = a.hd;
+    const int G = a.H / a.KVH, hd = a.hd, ndc = (hd + 31) / 32;
     const int L = __ldcg(P.state + 1);
     const int p0 = ch * a.chunk;
     const int p1 = min(L, p0 + a.chunk);
@@ -421,60 +533,74 @@ __device__ void attn_unit_t(const teal_step_plan& P, const teal_step_attn& a, co
     const int rec = G * hd + 2 * G;
     float* my = a.partials + ((int64_t)g * a.nchunks + ch) * rec;
     const int64_t kvbase = (int64_t)g * a.max_seq * hd;
+    unsigned long long* dbg = a.dbg ? a.dbg + ((int64_t)g * a.nchunks + ch) * 6 : nullptr;
+#define ATT_STAMP(k) do { if (dbg && tid == 0) dbg[k] = gtimer(); } while (0)
+    ATT_STAMP(0);
     if (np > 0) {
+        // stage q, and the chunk's K and V rows (contiguous in the cache), with
+        // 16-byte loads all in flight together: one L2/HBM round trip
+        constexpr int KB = (int)sizeof(KT);
+        const int n16 = np * hd * KB / 16;
+        const uint4* gk = reinterpret_cast<const uint4*>(reinterpret_cast<const KT*>(a.k_cache) + kvbase + (int64_t)p0 * hd);
+        const uint4* gv = reinterpret_cast<const uint4*>(reinterpret_cast<const KT*>(a.v_cache) + kvbase + (int64_t)p0 * hd);
         for (int o = tid; o < G * hd; o += NT) s.u.a.q[o] = __ldcg(a.q + (int64_t)g * G * hd + o);
+#pragma unroll 1
+        for (int v = tid; v < n16; v += 2 * NT) {
+            const uint4 k0 = __ldcg(gk + v), v0 = __ldcg(gv + v);
+            uint4 k1 = make_uint4(0u, 0u, 0u, 0u), v1 = k1;
+            if (v + NT < n16) { k1 = __ldcg(gk + v + NT); v1 = __ldcg(gv + v + NT); }
+            s.u.a.k[v] = k0;
+            s.u.a.v[v] = v0;
+            if (v + NT < n16) { s.u.a.k[v + NT] = k1; s.u.a.v[v + NT] = v1; }
+        }
         __syncthreads();
+        const KT* ks = reinterpret_cast<const KT*>(s.u.a.k);
+        const KT* vs = reinterpret_cast<const KT*>(s.u.a.v);
         const float den = sqrtf((float)hd);
+        // scores: warp per position, lanes over head_dim
+#pragma unroll 1
         for (int p = warp; p < np; p += NW) {
-            const int64_t krow = kvbase + (int64_t)(p0 + p) * hd;
-            float dot[ATT_MAXG];
+            float kr[ATT_MAXHD / 32];
 #pragma unroll
-            for (int h = 0; h < ATT_MAXG; ++h) dot[h] = 0.f;
-            for (int d = lane; d < hd; d += 32) {
-                const float kv = ld_kv<KT>(a.k_cache, krow + d);
+            for (int dc = 0; dc < ATT_MAXHD / 32; ++dc)
+                kr[dc] = (dc < ndc && lane + 32 * dc < hd) ? to_f32<KT>(ks[p * hd + lane + 32 * dc]) : 0.f;
+#pragma unroll 1
+            for (int h = 0; h < G; ++h) {
+                float dot = 0.f;
 #pragma unroll
-                for (int h = 0; h < ATT_MAXG; ++h)
-                    if (h < G) dot[h] = fmaf(s.u.a.q[h * hd + d], kv, dot[h]);
-            }
-#pragma unroll
-            for (int h = 0; h < ATT_MAXG; ++h) {
-                if (h < G) {
-                    const float sv = warp_sum(dot[h]);
-                    if (lane == 0) s.u.a.sc[h * ATT_MAXCHUNK + p] = sv / den;
-                }
+                for (int dc = 0; dc < ATT_MAXHD / 32; ++dc)
+                    if (dc < ndc && lane + 32 * dc < hd) dot = fmaf(s.u.a.q[h * hd + lane + 32 * dc], kr[dc], dot);
+                dot = warp_sum(dot);
+                if (lane == 0) s.u.a.sc[h * ATT_MAXCHUNK + p] = dot / den;
             }
         }
         __syncthreads();
-        if (warp < G) {
+        ATT_STAMP(1);
+        // softmax statistics: warp per head
+#pragma unroll 1
+        for (int h = warp; h < G; h += NW) {
             float mx = -INFINITY;
-            for (int p = lane; p < np; p += 32) mx = fmaxf(mx, s.u.a.sc[warp * ATT_MAXCHUNK + p]);
+            for (int p = lane; p < np; p += 32) mx = fmaxf(mx, s.u.a.sc[h * ATT_MAXCHUNK + p]);
             mx = warp_max(mx);
             float l = 0.f;
             for (int p = lane; p < np; p += 32) {
-                const float e = expf(s.u.a.sc[warp * ATT_MAXCHUNK + p] - mx);
-                s.u.a.sc[warp * ATT_MAXCHUNK + p] = e;
+                const float e = expf(s.u.a.sc[h * ATT_MAXCHUNK + p] - mx);
+                s.u.a.sc[h * ATT_MAXCHUNK + p] = e;
                 l += e;
             }
             l = warp_sum(l);
-            if (lane == 0) { s.am[warp] = mx; s.al[warp] = l; }
+            if (lane == 0) { s.am[h] = mx; s.al[h] = l; }
         }
         __syncthreads();
-        // context partial: thread -> (d, head set); positions ascending
-        const int hsets = NT / hd > 0 ? NT / hd : 1;
-        const int d = tid % hd, hs = tid / hd;
-        if (hs < hsets && d < hd) {
-            float accv[ATT_MAXG];
-#pragma unroll
-            for (int h = 0; h < ATT_MAXG; ++h) accv[h] = 0.f;
-            for (int p = 0; p < np; ++p) {
-                const float vv = ld_kv<KT>(a.v_cache, kvbase + (int64_t)(p0 + p) * hd + d);
-#pragma unroll
-                for (int h = 0; h < ATT_MAXG; ++h)
-                    if (h % hsets == hs && h < G) accv[h] = fmaf(s.u.a.sc[h * ATT_MAXCHUNK + p], vv, accv[h]);
-            }
-#pragma unroll
-            for (int h = 0; h < ATT_MAXG; ++h)
-                if (h % hsets == hs && h < G) __stcg(my + h * hd + d, accv[h]);
+        // context partial: thread -> (head, d), positions ascending
+#pragma unroll 1
+        for (int o = tid; o < G * hd; o += NT) {
+            const int h = o / hd, d = o - h * hd;
+            const float* pr = s.u.a.sc + h * ATT_MAXCHUNK;
+            float acc = 0.f;
+#pragma unroll 4
+            for (int p = 0; p < np; ++p) acc = fmaf(pr[p], to_f32<KT>(vs[p * hd + d]), acc);
+            __stcg(my + o, acc);
         }
         if (tid < G) {
             __stcg(my + G * hd + tid, s.am[tid]);
@@ -484,109 +610,171 @@ __device__ void attn_unit_t(const teal_step_plan& P, const teal_step_attn& a, co
         __stcg(my + G * hd + tid, -INFINITY);
         __stcg(my + G * hd + G + tid, 0.f);
     }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-        const unsigned prev = atomicAdd(a.tickets + g, 1u);
-        const int last = prev == (unsigned)a.nchunks - 1u;
-        if (last) a.tickets[g] = 0u;
-        s.last = last;
+    ATT_STAMP(2);
+    const bool last = take_ticket(a.tickets + g, (unsigned)a.nchunks - 1u, s.last);
+    ATT_STAMP(3);
+    if (!last) return;
+    const float* rb = a.partials + (int64_t)g * a.nchunks * rec;
+    const int nact = min(a.nchunks, (L + a.chunk - 1) / a.chunk);  // chunks holding positions
+    for (int q = tid; q < nact * 2 * G; q += NT) {  // (m, l) of every active chunk -> smem
+        const int c = q / (2 * G), k = q % (2 * G);
+        s.u.a.sc[q] = __ldcg(rb + (int64_t)c * rec + G * hd + k);
     }
     __syncthreads();
-    if (!s.last) return;
-    __threadfence();
-    const float* rb = a.partials + (int64_t)g * a.nchunks * rec;
+#pragma unroll 1
     for (int o = tid; o < G * hd; o += NT) {
         const int h = o / hd;
         float M = -INFINITY;
-        for (int c = 0; c < a.nchunks; ++c) {
-            const float* r = rb + (int64_t)c * rec;
-            if (__ldcg(r + G * hd + G + h) > 0.f) M = fmaxf(M, __ldcg(r + G * hd + h));
-        }
+        for (int c = 0; c < nact; ++c)
+            if (s.u.a.sc[c * 2 * G + G + h] > 0.f) M = fmaxf(M, s.u.a.sc[c * 2 * G + h]);
         float num = 0.f, dd = 0.f;
-        for (int c = 0; c < a.nchunks; ++c) {
-            const float* r = rb + (int64_t)c * rec;
-            const float ls = __ldcg(r + G * hd + G + h);
-            if (ls > 0.f) {
-                const float sc = expf(__ldcg(r + G * hd + h) - M);
-                num = fmaf(__ldcg(r + o), sc, num);
-                dd = fmaf(ls, sc, dd);
+#pragma unroll 1
+        for (int c0 = 0; c0 < nact; c0 += 4) {
+            float pv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pv[q] = (c0 + q < nact) ? __ldcg(rb + (int64_t)(c0 + q) * rec + o) : 0.f;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int c = c0 + q;
+                if (c < nact) {
+                    const float ls = s.u.a.sc[c * 2 * G + G + h];
+                    if (ls > 0.f) {
+                        const float sc = expf(s.u.a.sc[c * 2 * G + h] - M);
+                        num = fmaf(pv[q], sc, num);
+                        dd = fmaf(ls, sc, dd);
+                    }
+                }
             }
         }
         a.ctx[(int64_t)g * G * hd + o] = num / dd;
     }
+    ATT_STAMP(4);
     signal(P.counters, a.sig_base + g, a.sig_base + g);
+    ATT_STAMP(5);
+#undef ATT_STAMP
+}
+
+__device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, Smem& s) {
+    const teal_step_attn& a = P.attns[ph.group];
+    const int nu = a.KVH * a.nchunks;
+    const int G = gridDim.x;
+    // unit u runs on CTA (u * G) / nu: spread over the grid (different SMs)
+    for (int u = (int)(((int64_t)blockIdx.x * nu + G - 1) / G); u < nu && (int64_t)u * G / nu == blockIdx.x; ++u) {
+        const int g = u / a.nchunks, ch = u % a.nchunks;
+        wait_range(P.counters, a.dep_base + g, a.dep_base + g, a.dep_target[g]);
+        if (a.kv_dtype == TEAL_BF16) attn_unit_t<uint16_t>(P, a, g, ch, s);
+        else attn_unit_t<float>(P, a, g, ch, s);
+        __syncthreads();
+    }
 }
 
 // ---- residual load: x = emb[token] (or x_in); ss partials; {pos, len} ---------
-__device__ void load_unit(const teal_step_plan& P, Smem& s) {
-    const int tid = threadIdx.x;
+__device__ __noinline__ void load_phase(const teal_step_plan& P, Smem& s) {
+    if (blockIdx.x != 0) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         const int len = P.state[1];
         P.state[0] = len;
         P.state[1] = len + 1;
     }
     const int tok = P.emb ? __ldcg(P.token) : 0;
-    for (int t = 0; t < P.d / TW; ++t) {
-        const int64_t c = (int64_t)t * TW + tid;
-        float xv;
-        if (P.emb) {
-            const int64_t off = (int64_t)tok * P.d + c;
-            xv = P.emb_dtype == TEAL_BF16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(P.emb)[off])
-                                          : reinterpret_cast<const float*>(P.emb)[off];
-        } else {
-            xv = __ldcg(P.x_in + c);
+    const int nt = P.d / TW;  // <= NT tiles (d <= 65536)
+    // every column this thread owns is loaded before any is used
+#pragma unroll 1
+    for (int t0 = 0; t0 < nt; t0 += 16) {
+        float xv[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            xv[q] = 0.f;
+            if (t0 + q < nt) {
+                const int64_t c = (int64_t)(t0 + q) * TW + tid;
+                if (P.emb) {
+                    const int64_t off = (int64_t)tok * P.d + c;
+                    xv[q] = P.emb_dtype == TEAL_BF16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(P.emb)[off])
+                                                     : reinterpret_cast<const float*>(P.emb)[off];
+                } else {
+                    xv[q] = __ldcg(P.x_in + c);
+                }
+            }
         }
-        P.x[c] = xv;
-        const float ss = block_sum_nt(xv * xv, s);
-        if (tid == 0) P.ss[t] = ss;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            if (t0 + q < nt) P.x[(int64_t)(t0 + q) * TW + tid] = xv[q];
+            const float w = warp_sum(xv[q] * xv[q]);
+            if (lane == 0) s.red[warp * TW + q] = w;
+        }
+        __syncthreads();
+        if (tid < 16 && t0 + tid < nt) {  // per tile: warps summed in ascending order
+            float a = 0.f;
+            for (int w = 0; w < NW; ++w) a += s.red[w * TW + tid];
+            P.ss[t0 + tid] = a;
+        }
+        __syncthreads();
     }
     signal(P.counters, 0, 0);
 }
 
-template <int ESZ>
-__global__ void __launch_bounds__(NT, 3) step_kernel(const __grid_constant__ teal_step_plan P) {
-    __shared__ Smem s;
+// MINB resident CTAs per SM (register budget 65536 / (NT * MINB)); UB rows in
+// flight per warp per pipeline stage.
+template <int ESZ, int MINB, int UB>
+__global__ void __launch_bounds__(NT, MINB) step_kernel(const __grid_constant__ teal_step_plan P) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem& s = *reinterpret_cast<Smem*>(smem_raw);
     const int tid = threadIdx.x;
-    if (tid == 0) s.next = (int)atomicAdd(P.ctrl, 1u);
-    for (;;) {
+    const uint64_t pol = l2_evict_first_policy();
+    for (int p = 0; p < P.nphases; ++p) {
+        const teal_step_phase ph = P.phases[p];
+        unsigned long long* tl = P.timeline ? P.timeline + ((int64_t)blockIdx.x * P.nphases + p) * 8 : nullptr;
+        if (tl && tid == 0) tl[0] = gtimer();
+        if (ph.kind == TEAL_PHASE_GEMV) gemv_slice<ESZ, UB>(P, ph, s, pol, tl);
+        else if (ph.kind == TEAL_PHASE_ATTN) attn_phase(P, ph, s);
+        else load_phase(P, s);
         __syncthreads();
-        const int u = s.next;
-        if (u >= P.nunits) break;
-        __syncthreads();
-        if (tid == 0) s.next = (int)atomicAdd(P.ctrl, 1u);  // prefetch the next index
-        const teal_step_unit U = P.units[u];
-        if (U.dep >= 0) wait_counter(P.counters + U.dep, U.target);
-        if (U.kind == TEAL_UNIT_GEMV) {
-            gemv_unit<ESZ>(P, P.groups[U.group], U, s);
-        } else if (U.kind == TEAL_UNIT_ATTN) {
-            const teal_step_attn& a = P.attns[U.group];
-            if (a.kv_dtype == TEAL_BF16) attn_unit_t<uint16_t>(P, a, U, s);
-            else attn_unit_t<float>(P, a, U, s);
-        } else {
-            load_unit(P, s);
-        }
+        if (tl && tid == 0) tl[1] = gtimer();
     }
     if (tid == 0) {
         __threadfence();
-        const unsigned prev = atomicAdd(P.ctrl + 1, 1u);
+        const unsigned prev = atomicAdd(P.ctrl, 1u);
         if (prev == gridDim.x - 1u) {
-            for (int i = 0; i < P.ncounters; ++i) P.counters[i] = 0;
+            for (int i = 0; i < P.ncounters; ++i) P.counters[(int64_t)i * CSTRIDE] = 0;
             P.ctrl[0] = 0u;
-            P.ctrl[1] = 0u;
             __threadfence();
         }
     }
 }
 
+// Kernel variant: default 2 CTAs/SM with 8 rows per pipeline stage (128
+// registers, no spills in the streaming loop); TEAL_STEP_OCC=3 selects 3
+// CTAs/SM with 4 rows per stage (80 registers; measured slower: spills).
+static int occ_mode() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TEAL_STEP_OCC");
+        v = (e && e[0] == '3') ? 3 : 2;
+    }
+    return v;
+}
+
+template <int ESZ>
+static void* kernel_ptr() {
+    if (occ_mode() == 2) return (void*)step_kernel<ESZ, 2, 8>;
+    return (void*)step_kernel<ESZ, 3, 4>;
+}
+
 template <int ESZ>
 static int occupancy() {
-    int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, step_kernel<ESZ>, NT, 0) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
+    static int cached = -1;
+    if (cached < 0) {
+        const void* k = kernel_ptr<ESZ>();
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        int b = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, NT, kSmemBytes) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        cached = b;
     }
-    return b;
+    return cached;
 }
 
 }  // namespace step
@@ -604,9 +792,9 @@ int teal_step_ctas_per_sm(int w_dtype) {
 }
 
 int teal_step_launch(const teal_step_plan* p, cudaStream_t stream) {
-    TEAL_REQUIRE(p && p->groups && p->units && p->counters && p->ctrl && p->x && p->ss && p->state,
+    TEAL_REQUIRE(p && p->groups && p->phases && p->counters && p->ctrl && p->x && p->ss && p->state,
                  "teal_step_launch: null plan field");
-    TEAL_REQUIRE(p->nunits >= 1 && p->ncounters >= 1, "teal_step_launch: empty plan");
+    TEAL_REQUIRE(p->nphases >= 1 && p->ncounters >= 1, "teal_step_launch: empty plan");
     TEAL_REQUIRE(p->d >= TW && p->d % TW == 0, "teal_step_launch: d must be a multiple of %d", TW);
     TEAL_REQUIRE(p->w_dtype == TEAL_BF16 || p->w_dtype == TEAL_F32, "teal_step_launch: weights must be bf16 or fp32");
     int dev = 0, sms = 0;
@@ -614,20 +802,20 @@ int teal_step_launch(const teal_step_plan* p, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int per = teal_step_ctas_per_sm(p->w_dtype);
     TEAL_REQUIRE(per >= 1, "teal_step_launch: kernel cannot be resident");
-    int ctas = per * sms;
-    if (p->ctas > 0 && p->ctas < ctas) ctas = p->ctas;
+    TEAL_REQUIRE(p->ctas >= 1 && p->ctas <= per * sms,
+                 "teal_step_launch: plan built for %d CTAs, %d resident", p->ctas, per * sms);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ctas);
+    cfg.gridDim = dim3(p->ctas);
     cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = kSmemBytes;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (p->w_dtype == TEAL_BF16) cudaLaunchKernelEx(&cfg, step_kernel<2>, *p);
-    else cudaLaunchKernelEx(&cfg, step_kernel<4>, *p);
+    void* args[1] = {(void*)p};
+    cudaLaunchKernelExC(&cfg, p->w_dtype == TEAL_BF16 ? kernel_ptr<2>() : kernel_ptr<4>(), args);
     return check_launch("teal_step_launch");
 }
 

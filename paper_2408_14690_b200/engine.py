@@ -29,7 +29,6 @@ from .decode import PROJ, DecoderWeights, StepTaps, _t32
 
 TW = 256
 TH = TW // 2
-UNIT_LOAD, UNIT_GEMV, UNIT_ATTN = 0, 1, 2
 SEPI_STORE, SEPI_RESID, SEPI_SILU, SEPI_QKV, SEPI_LOGITS = 0, 1, 2, 3, 4
 
 c_i64, c_vp, c_f, c_i = ctypes.c_int64, ctypes.c_void_p, ctypes.c_float, ctypes.c_int
@@ -45,7 +44,7 @@ class StepGroup(ctypes.Structure):
                 ("partials", c_vp), ("tickets", c_vp), ("y", c_vp), ("resid", c_vp), ("ss_out", c_vp),
                 ("inter", c_vp), ("q_out", c_vp), ("k_cache", c_vp), ("v_cache", c_vp), ("rope_cos", c_vp),
                 ("rope_sin", c_vp), ("dbg_h", c_vp), ("dbg_bits", c_vp * 3), ("kept", c_vp * 3),
-                ("max_seq", c_i64), ("m", c_i), ("n", c_i), ("ntiles", c_i), ("nsplit", c_i),
+                ("max_seq", c_i64), ("m", c_i), ("n", c_i), ("ntiles", c_i), ("maxc", c_i),
                 ("prologue", c_i), ("nss", c_i), ("eps", c_f), ("epilogue", c_i),
                 ("nq", c_i), ("nkv", c_i), ("head_dim", c_i), ("kv_dtype", c_i), ("pad_", c_i)]
 
@@ -53,14 +52,35 @@ class StepGroup(ctypes.Structure):
 class StepAttn(ctypes.Structure):
     _fields_ = [("q", c_vp), ("k_cache", c_vp), ("v_cache", c_vp), ("ctx", c_vp), ("partials", c_vp),
                 ("tickets", c_vp), ("max_seq", c_i64), ("H", c_i), ("KVH", c_i), ("hd", c_i), ("kv_dtype", c_i),
-                ("chunk", c_i), ("nchunks", c_i), ("sig_base", c_i), ("pad_", c_i)]
+                ("chunk", c_i), ("nchunks", c_i), ("sig_base", c_i), ("dep_base", c_i), ("dep_target", c_vp),
+                ("dbg", c_vp)]
+
+
+class StepPhase(ctypes.Structure):
+    _fields_ = [("kind", c_i), ("group", c_i), ("dep_kind", c_i), ("dep", c_i), ("target", c_i), ("dep_rows", c_i)]
 
 
 class StepPlan(ctypes.Structure):
-    _fields_ = [("groups", c_vp), ("attns", c_vp), ("units", c_vp), ("counters", c_vp), ("ctrl", c_vp),
+    _fields_ = [("groups", c_vp), ("attns", c_vp), ("phases", c_vp), ("counters", c_vp), ("ctrl", c_vp),
                 ("emb", c_vp), ("x_in", c_vp), ("token", c_vp), ("x", c_vp), ("ss", c_vp), ("state", c_vp),
-                ("cand_v", c_vp), ("cand_i", c_vp), ("token_out", c_vp), ("lm_done", c_vp),
-                ("nunits", c_i), ("ncounters", c_i), ("d", c_i), ("emb_dtype", c_i), ("w_dtype", c_i), ("ctas", c_i)]
+                ("cand_v", c_vp), ("cand_i", c_vp), ("token_out", c_vp), ("lm_done", c_vp), ("timeline", c_vp),
+                ("nphases", c_i), ("ncounters", c_i), ("d", c_i), ("emb_dtype", c_i), ("w_dtype", c_i), ("ctas", c_i)]
+
+
+PHASE_LOAD, PHASE_GEMV, PHASE_ATTN = 0, 1, 2
+DEP_NONE, DEP_GLOBAL, DEP_ROWS = 0, 1, 2
+
+
+def max_contributors(ntiles: int, m: int, G: int) -> int:
+    """Most CTAs sharing one tile under the equal-range split of the
+    flattened (tile, 32-row group) space (csrc/teal_step.cu owner_of)."""
+    gpt = -(-m // 32)
+    F = ntiles * gpt
+    G = min(G, F)
+
+    def owner(x):
+        return ((x + 1) * G - 1) // F
+    return max(owner((t + 1) * gpt - 1) - owner(t * gpt) + 1 for t in range(ntiles))
 
 
 _BOUND = False
@@ -105,17 +125,6 @@ def pack_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor, tw: int = TW) -> torc
     return out
 
 
-def _splits(m: int, rows: int) -> list[tuple[int, int]]:
-    """K-ranges of at most `rows` rows (multiples of 32, balanced)."""
-    n = max(1, -(-m // rows))
-    per = -(-(-(-m // n)) // 32) * 32
-    out, r = [], 0
-    while r < m:
-        out.append((r, min(m, r + per)))
-        r += per
-    return out
-
-
 class StepDecoder:
     """TEAL decode for one sequence with one persistent launch per token.
 
@@ -124,8 +133,8 @@ class StepDecoder:
     dense for that projection)."""
 
     def __init__(self, weights: DecoderWeights, thresholds=None, kv_dtype=None, device=None,
-                 taps: bool = False, rows_per_unit: int = 512, attn_chunk: int = 256, ctas: int = 0,
-                 count_kept: bool = False):
+                 taps: bool = False, attn_chunk: int = 0, ctas: int = 0,
+                 count_kept: bool = False, attn_debug: bool = False):
         self.w = weights
         spec = self.spec = weights.spec
         dev = self.device = device or RT.require_cuda()
@@ -137,9 +146,11 @@ class StepDecoder:
             raise ValueError(f"StepDecoder needs d, n_q, n_kv multiples of {TW}, head_dim | {TW}, d_ff multiple of {TH}")
         if G > 8 or hd > 128 or G * hd > 1024:
             raise ValueError("StepDecoder attention supports <= 8 q heads per kv head and head_dim <= 128")
-        if attn_chunk > 256:
-            raise ValueError("attn_chunk must be <= 256")
-        self.rows_per_unit = min(1024, max(32, rows_per_unit // 32 * 32))
+        kvb = torch.empty(0, dtype=kv_dtype or weights.dtype).element_size()
+        stage_max = 16384 // (hd * kvb)  # positions whose K (and V) rows fit the kernel's staging buffer
+        attn_chunk = attn_chunk or stage_max
+        if not 1 <= attn_chunk <= min(256, stage_max):
+            raise ValueError(f"attn_chunk must be in [1, {min(256, stage_max)}]")
         self.kv_dtype = kv_dtype or weights.dtype
         self.w_dtype = weights.dtype
         f32 = dict(device=dev, dtype=torch.float32)
@@ -180,6 +191,7 @@ class StepDecoder:
         # kept-channel counters accumulated over every step (for algorithmic bytes)
         self.kept = self.taps.kept if taps else (torch.zeros(L, 7, device=dev, dtype=torch.int64) if count_kept else None)
         self.ctas = ctas
+        self.attn_dbg = torch.zeros(spec.n_kv_heads * self.nchunks, 6, device=dev, dtype=torch.int64) if attn_debug else None
         self._build(thresholds)
         self.graph = None
 
@@ -193,54 +205,49 @@ class StepDecoder:
         if len(thr) != L or any(len(t) != 7 for t in thr):
             raise ValueError(f"need {L} per-layer threshold lists of 7 (q,k,v,o,gate,up,down)")
         self.thresholds = thr
-        R = self.rows_per_unit
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        per = C.lib().teal_step_ctas_per_sm(RT.dtype_code(self.w_dtype))
+        if per < 1:
+            raise RuntimeError("teal step kernel cannot be resident on this device")
+        self.grid = min(self.ctas, per * sms) if self.ctas > 0 else per * sms
+        Gc = self.grid
         nt_qkv, nt_o, nt_gu, nt_dn = (nq + 2 * nkv) // TW, d // TW, f // TH, d // TW
-        sp_qkv = _splits(d, R)
-        sp_o = [(g * G * hd, (g + 1) * G * hd) for g in range(KVH)]
-        sp_gu = _splits(d, R)
-        KC = max(TH, (R // TH) * TH)                      # down K-chunk: whole gate/up tiles
-        sp_dn = [(r, min(f, r + KC)) for r in range(0, f, KC)]
-        # counters
-        per_layer = 2 * KVH + 1 + len(sp_dn) + 1
+        # counters: 0 load; per layer: attn deps [KVH], ctx ready [KVH], o done, gate/up tiles [nt_gu], down done
+        per_layer = 2 * KVH + 1 + nt_gu + 1
         self.ncounters = 1 + per_layer * L
 
         def cbase(l):
             b = 1 + per_layer * l
-            return dict(attn=b, odep=b + KVH, odone=b + 2 * KVH, gu=b + 2 * KVH + 1,
-                        down=b + 2 * KVH + 1 + len(sp_dn))
+            return dict(attn=b, odep=b + KVH, odone=b + 2 * KVH, gu=b + 2 * KVH + 1, down=b + 2 * KVH + 1 + nt_gu)
 
-        # workspaces (shared by the same group kind across layers)
-        self.ws = {
-            "qkv": torch.zeros(nt_qkv * len(sp_qkv) * TW, device=dev),
-            "o": torch.zeros(nt_o * len(sp_o) * TW, device=dev),
-            "gu": torch.zeros(nt_gu * len(sp_gu) * TW, device=dev),
-            "down": torch.zeros(nt_dn * len(sp_dn) * TW, device=dev),
-        }
-        self.tk = {k: torch.zeros(4096, device=dev, dtype=torch.int32) for k in ("qkv", "o", "gu", "down", "lm", "attn")}
+        mc = {"qkv": max_contributors(nt_qkv, d, Gc), "o": max_contributors(nt_o, nq, Gc),
+              "gu": max_contributors(nt_gu, d, Gc), "down": max_contributors(nt_dn, f, Gc)}
+        nts = {"qkv": nt_qkv, "o": nt_o, "gu": nt_gu, "down": nt_dn}
+        self.ws = {k: torch.zeros(nts[k] * mc[k] * TW, device=dev) for k in nts}
+        self.tk = {k: torch.zeros(max(4096, nts.get(k, 0)), device=dev, dtype=torch.int32)
+                   for k in ("qkv", "o", "gu", "down", "lm", "attn")}
         rec = G * hd + 2 * G
         self.ws["attn"] = torch.zeros(KVH * self.nchunks * rec, device=dev)
 
-        groups, attns, units, tiles_all = [], [], [], []
-        T = self.taps
-        K = self.kept
+        groups, attns, phases, keep = [], [], [], []
+        T, K = self.taps, self.kept
 
-        def tiles_tensor(meta):
-            arr = (StepTile * len(meta))(*meta)
+        def dev_bytes(arr):
             t = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(dev)
-            tiles_all.append(t)
+            keep.append(t)
             return t
 
-        def tile(tlo, thi, slo, shi, flo, fhi, s0, s1):
-            return StepTile(tlo, thi, slo, shi, flo, fhi, s0, s1)
+        def tiles_tensor(meta):
+            return dev_bytes((StepTile * len(meta))(*meta))
 
-        units.append((UNIT_LOAD, 0, 0, 0, 0, 0, -1, 0))
+        phases.append(StepPhase(PHASE_LOAD, 0, DEP_NONE, 0, 0, 1))
         for l, t in enumerate(thr):
             cb = cbase(l)
             tw = self.tw[l]
             lw = self.w.layers[l]
             kc, vc = self.kcache[l], self.vcache[l]
             dep_in = (0, 1) if l == 0 else (cbase(l - 1)["down"], nt_dn)
-            # --- qkv
+            # --- qkv: RMSNorm(x) -> 3 thresholds -> q (RoPE), k (RoPE) -> cache, v -> cache
             meta, feeds = [], [0] * KVH
             for ti in range(nt_qkv):
                 c0, c1 = ti * TW, ti * TW + TW - 1
@@ -254,99 +261,74 @@ class StepDecoder:
                 for gg in range(g0, g1 + 1):
                     feeds[gg] += 1
                 tv = _t32(t[seg])
-                meta.append(tile(tv, tv, seg, seg, int(first), int(first), cb["attn"] + g0, cb["attn"] + g1))
-            gq = self._group(tw["qkv"], tiles_tensor(meta), m=d, n=nq + 2 * nkv, nsplit=len(sp_qkv),
-                             x=self.x, gain=lw.rms_attn, prologue=C.PRO_RMSNORM, ws="qkv", epilogue=SEPI_QKV,
-                             q_out=self.q, k_cache=kc, v_cache=vc,
-                             dbg=(T.h["pre_attn"][l] if T else None,
-                                  [T.bits[p][l] for p in ("q", "k", "v")] if T else None,
-                                  [K[l, PROJ.index(p)] for p in ("q", "k", "v")] if K is not None else None))
-            gi = len(groups)
-            groups.append(gq)
-            for ti in range(nt_qkv):
-                for s, (r0, r1) in enumerate(sp_qkv):
-                    units.append((UNIT_GEMV, gi, ti, s, r0, r1, dep_in[0], dep_in[1]))
-            # --- attention
-            ai = len(attns)
+                meta.append(StepTile(tv, tv, seg, seg, int(first), int(first), cb["attn"] + g0, cb["attn"] + g1))
+            groups.append(self._group(tw["qkv"], tiles_tensor(meta), m=d, n=nq + 2 * nkv, maxc=mc["qkv"],
+                                      x=self.x, gain=lw.rms_attn, prologue=C.PRO_RMSNORM, ws="qkv",
+                                      epilogue=SEPI_QKV, q_out=self.q, k_cache=kc, v_cache=vc,
+                                      dbg=(T.h["pre_attn"][l] if T else None,
+                                           [T.bits[p][l] for p in ("q", "k", "v")] if T else None,
+                                           [K[l, PROJ.index(p)] for p in ("q", "k", "v")] if K is not None else None)))
+            phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_GLOBAL, dep_in[0], dep_in[1], 1))
+            # --- attention per (kv group, position chunk)
+            tgt = torch.tensor(feeds, dtype=torch.int32, device=dev)
+            keep.append(tgt)
             attns.append(StepAttn(self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(), self.ctx.data_ptr(),
                                   self.ws["attn"].data_ptr(), self.tk["attn"].data_ptr(), spec.max_seq,
                                   spec.n_heads, KVH, hd, RT.dtype_code(self.kv_dtype), self.attn_chunk,
-                                  self.nchunks, cb["odep"], 0))
-            for gg in range(KVH):
-                for c in range(self.nchunks):
-                    units.append((UNIT_ATTN, ai, gg, c, 0, 0, cb["attn"] + gg, feeds[gg]))
-            # --- o (K-split by kv group)
+                                  self.nchunks, cb["odep"], cb["attn"], tgt.data_ptr(), RT.ptr(self.attn_dbg)))
+            phases.append(StepPhase(PHASE_ATTN, len(attns) - 1, DEP_NONE, 0, 0, 1))
+            # --- o: rows = context channels, each waits for its kv group's context
             tv = _t32(t[3])
-            meta = [tile(tv, tv, 0, 0, int(ti == 0), int(ti == 0), cb["odone"], cb["odone"]) for ti in range(nt_o)]
-            go = self._group(tw["o"], tiles_tensor(meta), m=nq, n=d, nsplit=len(sp_o), x=self.ctx,
-                             prologue=C.PRO_PLAIN, ws="o", epilogue=SEPI_RESID,
-                             dbg=(T.h["attn_out"][l] if T else None, [T.bits["o"][l]] if T else None,
-                                  [K[l, 3]] if K is not None else None))
-            gi = len(groups)
-            groups.append(go)
-            for s, (r0, r1) in enumerate(sp_o):
-                for ti in range(nt_o):
-                    units.append((UNIT_GEMV, gi, ti, s, r0, r1, cb["odep"] + s, 1))
-            # --- gate/up
+            meta = [StepTile(tv, tv, 0, 0, int(ti == 0), int(ti == 0), cb["odone"], cb["odone"]) for ti in range(nt_o)]
+            groups.append(self._group(tw["o"], tiles_tensor(meta), m=nq, n=d, maxc=mc["o"], x=self.ctx,
+                                      prologue=C.PRO_PLAIN, ws="o", epilogue=SEPI_RESID,
+                                      dbg=(T.h["attn_out"][l] if T else None, [T.bits["o"][l]] if T else None,
+                                           [K[l, 3]] if K is not None else None)))
+            phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_ROWS, cb["odep"], 1, G * hd))
+            # --- gate/up: RMSNorm(x) after every o tile -> SiLU(gate)*up
             tg, tu = _t32(t[4]), _t32(t[5])
-            meta = []
-            for ti in range(nt_gu):
-                k = (ti * TH) // KC
-                meta.append(tile(tg, tu, 0, 1, int(ti == 0), int(ti == 0), cb["gu"] + k, cb["gu"] + k))
-            ggu = self._group(tw["gu"], tiles_tensor(meta), m=d, n=f, nsplit=len(sp_gu), x=self.x,
-                              gain=lw.rms_mlp, prologue=C.PRO_RMSNORM, ws="gu", epilogue=SEPI_SILU,
-                              dbg=(T.h["pre_mlp"][l] if T else None, [T.bits["gate"][l], T.bits["up"][l]] if T else None,
-                                   [K[l, 4], K[l, 5]] if K is not None else None))
-            gi = len(groups)
-            groups.append(ggu)
-            for ti in range(nt_gu):
-                for s, (r0, r1) in enumerate(sp_gu):
-                    units.append((UNIT_GEMV, gi, ti, s, r0, r1, cb["odone"], nt_o))
-            # --- down (K-chunks of whole gate/up tiles)
+            meta = [StepTile(tg, tu, 0, 1, int(ti == 0), int(ti == 0), cb["gu"] + ti, cb["gu"] + ti)
+                    for ti in range(nt_gu)]
+            groups.append(self._group(tw["gu"], tiles_tensor(meta), m=d, n=f, maxc=mc["gu"], x=self.x,
+                                      gain=lw.rms_mlp, prologue=C.PRO_RMSNORM, ws="gu", epilogue=SEPI_SILU,
+                                      dbg=(T.h["pre_mlp"][l] if T else None,
+                                           [T.bits["gate"][l], T.bits["up"][l]] if T else None,
+                                           [K[l, 4], K[l, 5]] if K is not None else None)))
+            phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_GLOBAL, cb["odone"], nt_o, 1))
+            # --- down: rows = intermediate channels, each waits for its gate/up tile
             tv = _t32(t[6])
-            meta = [tile(tv, tv, 0, 0, int(ti == 0), int(ti == 0), cb["down"], cb["down"]) for ti in range(nt_dn)]
-            gdn = self._group(tw["down"], tiles_tensor(meta), m=f, n=d, nsplit=len(sp_dn), x=self.inter,
-                              prologue=C.PRO_PLAIN, ws="down", epilogue=SEPI_RESID,
-                              dbg=(T.h["mlp_inter"][l] if T else None, [T.bits["down"][l]] if T else None,
-                                   [K[l, 6]] if K is not None else None))
-            gi = len(groups)
-            groups.append(gdn)
-            for k, (r0, r1) in enumerate(sp_dn):
-                need = (r1 - 1) // TH - r0 // TH + 1
-                for ti in range(nt_dn):
-                    units.append((UNIT_GEMV, gi, ti, k, r0, r1, cb["gu"] + k, need))
-        self.lm_group = None
+            meta = [StepTile(tv, tv, 0, 0, int(ti == 0), int(ti == 0), cb["down"], cb["down"]) for ti in range(nt_dn)]
+            groups.append(self._group(tw["down"], tiles_tensor(meta), m=f, n=d, maxc=mc["down"], x=self.inter,
+                                      prologue=C.PRO_PLAIN, ws="down", epilogue=SEPI_RESID,
+                                      dbg=(T.h["mlp_inter"][l] if T else None, [T.bits["down"][l]] if T else None,
+                                           [K[l, 6]] if K is not None else None)))
+            phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_ROWS, cb["gu"], 1, TH))
         if spec.vocab:
             nt_lm = self.lm_t.shape[0]
-            sp_lm = _splits(d, R)
-            self.ws["lm"] = torch.zeros(nt_lm * len(sp_lm) * TW, device=dev)
-            meta = [tile(float("-inf"), float("-inf"), 0, 0, 0, 0, -1, -1) for _ in range(nt_lm)]
-            glm = self._group(self.lm_t, tiles_tensor(meta), m=d, n=spec.vocab, nsplit=len(sp_lm), x=self.x,
-                              gain=self.w.final_norm, prologue=C.PRO_RMSNORM, ws="lm", epilogue=SEPI_LOGITS,
-                              y=self.logits)
-            gi = len(groups)
-            groups.append(glm)
-            last = cbase(L - 1)["down"]
-            for ti in range(nt_lm):
-                for s, (r0, r1) in enumerate(sp_lm):
-                    units.append((UNIT_GEMV, gi, ti, s, r0, r1, last, nt_dn))
-            self.cand_v = torch.zeros(nt_lm, **dict(device=dev, dtype=torch.float32))
+            mc_lm = max_contributors(nt_lm, d, Gc)
+            self.ws["lm"] = torch.zeros(nt_lm * mc_lm * TW, device=dev)
+            self.tk["lm"] = torch.zeros(max(4096, nt_lm), device=dev, dtype=torch.int32)
+            meta = [StepTile(float("-inf"), float("-inf"), 0, 0, 0, 0, -1, -1) for _ in range(nt_lm)]
+            groups.append(self._group(self.lm_t, tiles_tensor(meta), m=d, n=spec.vocab, maxc=mc_lm, x=self.x,
+                                      gain=self.w.final_norm, prologue=C.PRO_RMSNORM, ws="lm",
+                                      epilogue=SEPI_LOGITS, y=self.logits))
+            phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_GLOBAL, cbase(L - 1)["down"], nt_dn, 1))
+            self.cand_v = torch.zeros(nt_lm, device=dev)
             self.cand_i = torch.zeros(nt_lm, device=dev, dtype=torch.int32)
         else:
             self.cand_v = torch.zeros(1, device=dev)
             self.cand_i = torch.zeros(1, device=dev, dtype=torch.int32)
         self.lm_done = torch.zeros(1, device=dev, dtype=torch.int32)
-        self._tiles = tiles_all
-        garr = (StepGroup * len(groups))(*groups)
-        self._groups = torch.frombuffer(bytearray(bytes(garr)), dtype=torch.uint8).to(dev)
-        aarr = (StepAttn * len(attns))(*attns)
-        self._attns = torch.frombuffer(bytearray(bytes(aarr)), dtype=torch.uint8).to(dev)
-        self._units = torch.tensor(units, dtype=torch.int32).to(dev)
-        self.nunits = len(units)
-        self.counters = torch.zeros(self.ncounters, device=dev, dtype=torch.int32)
+        self._keep = keep
+        self._groups = dev_bytes((StepGroup * len(groups))(*groups))
+        self._attns = dev_bytes((StepAttn * len(attns))(*attns))
+        self._phases = dev_bytes((StepPhase * len(phases))(*phases))
+        self.nphases = len(phases)
+        self.counters = torch.zeros(self.ncounters * 32, device=dev, dtype=torch.int32)
         self.ctrl = torch.zeros(4, device=dev, dtype=torch.int32)
+        self.timeline = None
         p = StepPlan()
-        p.groups, p.attns, p.units = self._groups.data_ptr(), self._attns.data_ptr(), self._units.data_ptr()
+        p.groups, p.attns, p.phases = self._groups.data_ptr(), self._attns.data_ptr(), self._phases.data_ptr()
         p.counters, p.ctrl = self.counters.data_ptr(), self.ctrl.data_ptr()
         if spec.vocab:
             p.emb, p.emb_dtype = self.w.embedding.data_ptr(), RT.dtype_code(self.w.embedding.dtype)
@@ -354,12 +336,20 @@ class StepDecoder:
                                                self.ss.data_ptr(), self.state.data_ptr())
         p.cand_v, p.cand_i, p.token_out, p.lm_done = (self.cand_v.data_ptr(), self.cand_i.data_ptr(),
                                                       self.token.data_ptr(), self.lm_done.data_ptr())
-        p.nunits, p.ncounters, p.d = self.nunits, self.ncounters, d
-        p.w_dtype, p.ctas = RT.dtype_code(self.w_dtype), self.ctas
+        p.nphases, p.ncounters, p.d = self.nphases, self.ncounters, d
+        p.w_dtype, p.ctas = RT.dtype_code(self.w_dtype), self.grid
         self.plan = p
-        self.unit_counts = {"total": self.nunits}
 
-    def _group(self, wt, tiles, m, n, nsplit, x, prologue, ws, epilogue, gain=None, q_out=None, k_cache=None,
+    def enable_timeline(self) -> torch.Tensor:
+        """Debug: record %globaltimer at entry/exit of every phase of every CTA
+        ([grid, nphases, 8] int64, overwritten by each launch): 0 start, 1 end;
+        GEMV phases also 2 deps met, 3/5 first/second segment streamed, 4 first
+        segment finished, 6 segments, 7 tiles this CTA finalized."""
+        self.timeline = torch.zeros(self.grid, self.nphases, 8, device=self.device, dtype=torch.int64)
+        self.plan.timeline = self.timeline.data_ptr()
+        return self.timeline
+
+    def _group(self, wt, tiles, m, n, maxc, x, prologue, ws, epilogue, gain=None, q_out=None, k_cache=None,
                v_cache=None, y=None, dbg=None):
         spec = self.spec
         g = StepGroup()
@@ -380,7 +370,7 @@ class StepDecoder:
                 g.dbg_bits[i] = b.data_ptr()
             for i, k in enumerate(kept or []):
                 g.kept[i] = k.data_ptr()
-        g.max_seq, g.m, g.n, g.ntiles, g.nsplit = spec.max_seq, m, n, wt.shape[0], nsplit
+        g.max_seq, g.m, g.n, g.ntiles, g.maxc = spec.max_seq, m, n, wt.shape[0], maxc
         g.prologue, g.nss, g.eps, g.epilogue = prologue, spec.d_model // TW, spec.norm_eps, epilogue
         g.nq, g.nkv, g.head_dim, g.kv_dtype = spec.n_q, spec.n_kv, spec.head_dim, RT.dtype_code(self.kv_dtype)
         return g

@@ -16,7 +16,8 @@ from paper_2408_14690_b200 import engine as E  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=50)
-ap.add_argument("--rows", type=int, default=512)
+ap.add_argument("--ctas", type=int, default=0)
+ap.add_argument("--timeline", action="store_true")
 ap.add_argument("--layers", type=int, default=32)
 ap.add_argument("--engines", default="launch,step")
 a = ap.parse_args()
@@ -27,7 +28,7 @@ hists = D.calibrate_histograms(W, n_tokens=8)
 for s in (None, 0.5):
     thr = None if s is None else D.uniform_thresholds(hists, spec.n_layers, s)
     for eng in a.engines.split(","):
-        dec = (E.StepDecoder(W, thr, rows_per_unit=a.rows, count_kept=True) if eng == "step"
+        dec = (E.StepDecoder(W, thr, ctas=a.ctas, count_kept=True) if eng == "step"
                else D.SparseDecoder(W, thr))
         dec.reset()
         dec.capture()
@@ -49,5 +50,19 @@ for s in (None, 0.5):
             byts = dec.algorithmic_bytes(dec.kept, steps=a.steps) / a.steps
             extra = f" algo {byts / 1e9:.3f} GB/step -> {byts / (ms * 1e-3) / 1e9:.0f} GB/s"
         print(f"{eng:6s} s={s}: {ms:.3f} ms/token  {1e3 / ms:.1f} tok/s{extra}", flush=True)
+        if eng == "step" and a.timeline:
+            tl = dec.enable_timeline()
+            dec.capture()
+            dec.replay()
+            dec.replay()
+            torch.cuda.synchronize()
+            t = tl.cpu().double()
+            t0 = t[:, 0, 0].min()
+            t = (t - t0) / 1e3  # us
+            names = ["load"] + ["qkv", "attn", "o", "gu", "down"] * spec.n_layers + (["lm"] if spec.vocab else [])
+            for p_ in list(range(0, 11)) + list(range(len(names) - 6, len(names))):
+                st, en = t[:, p_, 0], t[:, p_, 1]
+                print(f"   phase {p_:3d} {names[p_]:5s} start min {st.min():8.1f} med {st.median():8.1f} max {st.max():8.1f}"
+                      f" | end min {en.min():8.1f} med {en.median():8.1f} max {en.max():8.1f}")
         del dec
         torch.cuda.empty_cache()
