@@ -45,6 +45,8 @@ extern "C" {
 #define TEAL_F32 0
 #define TEAL_BF16 1
 #define TEAL_I8 2       /* int8 rows, per-output-column fp32 scale */
+#define TEAL_I4 3       /* int4 rows (two per byte, low nibble = even column),
+                           fp32 scale per (group of input rows, column) */
 
 /* fused-GEMV prologues: how the input h is formed from x */
 #define TEAL_PRO_PLAIN 0     /* h_i = x_i */
@@ -149,6 +151,34 @@ int teal_sparse_gemv(const void* w, int w_dtype, int64_t m, int64_t n, int64_t l
 int teal_dense_gemv(const void* w, int w_dtype, int64_t m, int64_t n, int64_t ldw,
                     const void* x, int x_dtype, float* y, const float* col_scale,
                     float* ws, uint32_t* tickets, int ctas, cudaStream_t stream);
+
+
+/* ---- batched shared-mask sparse GEMV over bf16 / int8 / int4 rows ---------
+ * Replaces sparsify_batched followed by the dense product
+ * (sparsifier.py:136-155, tensor.py:130-140) for B <= 16 decode rows:
+ * column i is pruned in every row iff mean_b |x[b,i]| <= t32 (fp32 sum in
+ * ascending b, fp64 quotient rounded to fp32), and
+ * y[b] = sum over kept i of x[b,i] * W[i,:] — each kept row read once. */
+typedef struct teal_gemv_batched_args {
+    const void* w;               /* input-major rows, row stride ldw elements   */
+    const float* scale;          /* I8: [n]; I4: [ceil(m/group)][n]             */
+    const float* x;              /* [B][m] fp32                                 */
+    float* y;                    /* [B][n] fp32                                 */
+    uint8_t* mask;               /* nullable: [m], 1 = pruned                   */
+    unsigned long long* kept;    /* nullable: += kept input channels            */
+    float* ws;                   /* split-K partials (teal_gemv_batched_workspace) */
+    uint32_t* tickets;           /* zeroed, self-resetting                      */
+    int64_t m, n, ldw;
+    int w_dtype;                 /* TEAL_BF16 / TEAL_I8 / TEAL_I4               */
+    int group;                   /* I4 row-group size                           */
+    int B;                       /* 1..16                                       */
+    float t32;                   /* -INFINITY = dense                           */
+    int ctas;                    /* 0 = auto                                    */
+    int pad_;
+} teal_gemv_batched_args;
+
+int teal_gemv_batched_workspace(const teal_gemv_batched_args* a, int* ctas, int64_t* ws_floats, int64_t* tickets);
+int teal_gemv_batched(const teal_gemv_batched_args* a, cudaStream_t stream);
 
 /* ---- calibration ------------------------------------------------------- */
 

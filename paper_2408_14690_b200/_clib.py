@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "lib" / "libteal_b200.so"
 
 TEAL_OK, TEAL_EINVAL, TEAL_ECUDA = 0, 1, 2
-TEAL_F32, TEAL_BF16, TEAL_I8 = 0, 1, 2
+TEAL_F32, TEAL_BF16, TEAL_I8, TEAL_I4 = 0, 1, 2, 3
 PRO_PLAIN, PRO_RMSNORM = 0, 1
 EPI_STORE, EPI_RESID, EPI_SILU, EPI_QKV = 0, 1, 2, 3
 
@@ -45,6 +45,13 @@ class TealGemvArgs(ctypes.Structure):
     ]
 
 
+class TealGemvBatchedArgs(ctypes.Structure):
+    _fields_ = [("w", c_vp), ("scale", c_vp), ("x", c_vp), ("y", c_vp), ("mask", c_vp), ("kept", c_vp),
+                ("ws", c_vp), ("tickets", c_vp), ("m", c_i64), ("n", c_i64), ("ldw", c_i64),
+                ("w_dtype", ctypes.c_int), ("group", ctypes.c_int), ("B", ctypes.c_int), ("t32", ctypes.c_float),
+                ("ctas", ctypes.c_int), ("pad_", ctypes.c_int)]
+
+
 # (name, restype, argtypes) for every exported symbol of include/teal_b200.h
 _SIGNATURES = [
     ("teal_last_error", ctypes.c_char_p, []),
@@ -71,6 +78,9 @@ _SIGNATURES = [
     ("teal_load_residual", ctypes.c_int, [c_vp, ctypes.c_int, c_vp, c_i64, c_vp, c_vp, ctypes.c_int, c_vp, c_vp]),
     ("teal_argmax", ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     ("teal_step_ctas_per_sm", ctypes.c_int, [ctypes.c_int]),
+    ("teal_gemv_batched_workspace", ctypes.c_int, [ctypes.POINTER(TealGemvBatchedArgs), ctypes.POINTER(ctypes.c_int),
+                                                   ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
+    ("teal_gemv_batched", ctypes.c_int, [ctypes.POINTER(TealGemvBatchedArgs), c_vp]),
     ("teal_step_launch", ctypes.c_int, [c_vp, c_vp]),
 ]
 

@@ -1,0 +1,352 @@
+// Batched (B <= 16) shared-mask sparse GEMV over bf16 / int8 / int4 weight
+// rows (sm_100a) — BASELINE config 5 (small-batch decode with weight-quantized
+// rows).
+//
+// Semantics = the reference's batched sparsification followed by the dense
+// product (pkg/src/actsparse/sparsifier.py:136-155 `sparsify_batched`, then
+// tensor.py:130-140 `matmul_dense` per row):
+//   column i of X [B][m] is pruned in every row iff mean_b |X[b,i]| <= t
+//   (fp32 sum in ascending b, then the fp64 quotient rounded to fp32, exactly
+//   as teal_threshold_batched), and Y[b] = sum over kept i of X[b,i] * W[i,:].
+// Each kept input channel's weight row is read ONCE for all B batch rows.
+//
+// Weights (input-major, row i = n outputs, row stride ldw elements):
+//   bf16 ; int8 with a per-output-column fp32 scale (W = q * s[j]) ;
+//   int4 two's-complement nibbles, two per byte (low nibble = even column),
+//   with an fp32 scale per (group of `group` input rows, column):
+//   W[i,j] = q * s[i / group][j].
+//
+// Decomposition as teal_fused_gemv: the flattened (column tile, 32-row group)
+// space is cut into equal contiguous CTA ranges; a lane owns CPL consecutive
+// columns of a TC = 32*CPL column tile and all B batch rows (fp32
+// accumulators acc[B][CPL]); warps take kept rows round-robin with U rows in
+// flight; warps are reduced in fixed order, split tiles by the last-arriving
+// CTA in ascending-CTA order (deterministic).  CUDA cores only: at B >= 4 the
+// kernel is FMA-bound, at B = 1 the fused single-row kernels
+// are the fast path.
+#include "teal_common.cuh"
+#include <string.h>
+
+namespace teal {
+namespace batched {
+
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+constexpr int CHUNK = 256;   // rows compacted per round
+constexpr int BMAX = 16;
+
+// bytes of CPL consecutive elements of a row
+template <int WT, int CPL> struct RowLoad;
+template <int CPL> struct RowLoad<TEAL_BF16, CPL> { static constexpr int BYTES = 2 * CPL; };
+template <int CPL> struct RowLoad<TEAL_I8, CPL> { static constexpr int BYTES = CPL; };
+template <int CPL> struct RowLoad<TEAL_I4, CPL> { static constexpr int BYTES = CPL / 2; };
+
+template <int BYTES>
+__device__ __forceinline__ uint4 ld_row(const void* p) {
+    uint4 r = make_uint4(0u, 0u, 0u, 0u);
+    if constexpr (BYTES == 16) {
+        r = ldg128_stream(p);
+    } else if constexpr (BYTES == 8) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+        r.x = v.x;
+        r.y = v.y;
+    } else if constexpr (BYTES == 4) {
+        r.x = __ldg(reinterpret_cast<const unsigned int*>(p));
+    } else {
+        r.x = __ldg(reinterpret_cast<const unsigned short*>(p));
+    }
+    return r;
+}
+
+// dequantise CPL packed elements (without scale)
+template <int WT, int CPL>
+__device__ __forceinline__ void unpack(const uint4 d, float* w) {
+    const uint32_t u[4] = {d.x, d.y, d.z, d.w};
+    if constexpr (WT == TEAL_BF16) {
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) w[k] = (k & 1) ? bf16_hi(u[k >> 1]) : bf16_lo(u[k >> 1]);
+    } else if constexpr (WT == TEAL_I8) {
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) w[k] = (float)(int8_t)((u[k >> 2] >> (8 * (k & 3))) & 0xffu);
+    } else {
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+            const int nib = (int)((u[k >> 3] >> (4 * (k & 7))) & 0xfu);
+            w[k] = (float)(nib >= 8 ? nib - 16 : nib);
+        }
+    }
+}
+
+struct KP {
+    teal_gemv_batched_args a;
+    int gpt;        // 32-row groups per tile
+    int ntiles;
+    int64_t F;
+    int G;
+    int maxc;       // partial slots per tile
+};
+
+__host__ __device__ __forceinline__ int owner_of(int64_t g, int64_t F, int G) { return (int)(((g + 1) * G - 1) / F); }
+
+template <int WT, int BM, int CPL>
+__global__ void __launch_bounds__(NT, 2) gemv_batched_kernel(const __grid_constant__ KP P) {
+    constexpr int TC = 32 * CPL;
+    constexpr int LB = RowLoad<WT, CPL>::BYTES;
+    constexpr int U = 4;
+    __shared__ int s_idx[CHUNK];
+    __shared__ float s_x[CHUNK * BM];
+    __shared__ float s_red[BM * TC];
+    __shared__ int s_wcnt[NW];
+    __shared__ int s_last;
+    const teal_gemv_batched_args& A = P.a;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x;
+    const int64_t g0 = (int64_t)c * P.F / P.G, g1 = (int64_t)(c + 1) * P.F / P.G;
+    const int B = A.B;
+    unsigned kcount = 0;
+    for (int64_t gs = g0; gs < g1;) {
+        const int tile = (int)(gs / P.gpt);
+        const int64_t ge = min64(g1, (int64_t)(tile + 1) * P.gpt);
+        const int r0 = (int)(gs - (int64_t)tile * P.gpt) * 32;
+        const int r1 = (int)min64(A.m, (ge - (int64_t)tile * P.gpt) * 32);
+        gs = ge;
+        const int64_t col0 = (int64_t)tile * TC + lane * CPL;
+        float acc[BM][CPL];
+#pragma unroll
+        for (int b = 0; b < BM; ++b)
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) acc[b][k] = 0.f;
+        int sgrp = -1;
+        float sc[CPL];
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) sc[k] = 1.f;
+        for (int ra = r0; ra < r1; ra += CHUNK) {
+            const int rb = min(r1, ra + CHUNK);
+            // shared mask of this chunk (ordered compaction)
+            const int i = ra + tid;
+            const bool v = i < rb;
+            float xs[BM];
+            float s = 0.f;
+#pragma unroll
+            for (int b = 0; b < BM; ++b) {
+                xs[b] = (v && b < B) ? A.x[(int64_t)b * A.m + i] : 0.f;
+                if (b < B) s = __fadd_rn(s, fabsf(xs[b]));
+            }
+            const float mean = (float)__ddiv_rn((double)s, (double)B);
+            const bool keep = v && !(mean <= A.t32);
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (tile == 0) {
+                if (A.mask && v) A.mask[i] = keep ? 0 : 1;
+                kcount += (lane == 0) ? __popc(bal) : 0u;
+            }
+            if (lane == 0) s_wcnt[warp] = __popc(bal);
+            __syncthreads();
+            int off = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const int cw = s_wcnt[w];
+                off += (w < warp) ? cw : 0;
+                tot += cw;
+            }
+            if (keep) {
+                const int pos = off + __popc(bal & ((1u << lane) - 1u));
+                s_idx[pos] = i;
+#pragma unroll
+                for (int b = 0; b < BM; ++b) s_x[pos * BM + b] = xs[b];
+            }
+            __syncthreads();
+            // stream the kept rows: warp w takes entries w*U.., U rows in flight
+            for (int e0 = warp * U; e0 < tot; e0 += NW * U) {
+                uint4 d[U];
+                int rows[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int e = e0 + u;
+                    rows[u] = e < tot ? s_idx[e] : -1;
+                    d[u] = make_uint4(0u, 0u, 0u, 0u);
+                    if (rows[u] >= 0 && col0 < A.n) {
+                        const int64_t el = (int64_t)rows[u] * A.ldw + col0;
+                        const unsigned char* p = reinterpret_cast<const unsigned char*>(A.w) +
+                                                 (WT == TEAL_BF16 ? el * 2 : (WT == TEAL_I8 ? el : el / 2));
+                        d[u] = ld_row<LB>(p);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (rows[u] < 0) continue;
+                    float w[CPL];
+                    unpack<WT, CPL>(d[u], w);
+                    if constexpr (WT == TEAL_I4) {
+                        const int grp = rows[u] / A.group;
+                        if (grp != sgrp) {  // rows ascend: the group scale changes rarely
+                            sgrp = grp;
+#pragma unroll
+                            for (int k = 0; k < CPL; ++k)
+                                sc[k] = (col0 + k < A.n) ? __ldg(A.scale + (int64_t)grp * A.n + col0 + k) : 0.f;
+                        }
+#pragma unroll
+                        for (int k = 0; k < CPL; ++k) w[k] *= sc[k];
+                    }
+                    const float* xr = s_x + (e0 + u) * BM;
+#pragma unroll
+                    for (int b = 0; b < BM; ++b) {
+                        const float xb = xr[b];
+#pragma unroll
+                        for (int k = 0; k < CPL; ++k) acc[b][k] = fmaf(xb, w[k], acc[b][k]);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        // fixed-order warp reduction: warp 0 writes, warps 1..7 add in turn
+        for (int w = 0; w < NW; ++w) {
+            if (warp == w) {
+#pragma unroll
+                for (int b = 0; b < BM; ++b)
+#pragma unroll
+                    for (int k = 0; k < CPL; ++k) {
+                        float* r = s_red + b * TC + lane * CPL + k;
+                        *r = (w == 0) ? acc[b][k] : *r + acc[b][k];
+                    }
+            }
+            __syncthreads();
+        }
+        // split-K combine (ascending CTA order) + store
+        const int cf = owner_of((int64_t)tile * P.gpt, P.F, P.G);
+        const int cl = owner_of((int64_t)(tile + 1) * P.gpt - 1, P.F, P.G);
+        bool fin = true;
+        if (cl > cf) {
+            float* slot = A.ws + ((int64_t)tile * P.maxc + (c - cf)) * (BM * TC);
+            for (int q = tid; q < BM * TC; q += NT) __stcg(slot + q, s_red[q]);
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                const unsigned prev = atomicAdd(A.tickets + tile, 1u);
+                s_last = prev == (unsigned)(cl - cf);
+                if (s_last) {
+                    A.tickets[tile] = 0u;
+                    __threadfence();
+                }
+            }
+            __syncthreads();
+            fin = s_last != 0;
+            if (fin) {
+                const float* base = A.ws + (int64_t)tile * P.maxc * (BM * TC);
+                for (int q = tid; q < BM * TC; q += NT) {
+                    float v = 0.f;
+                    for (int k = 0; k <= cl - cf; ++k) v += __ldcg(base + (int64_t)k * (BM * TC) + q);
+                    s_red[q] = v;
+                }
+                __syncthreads();
+            }
+        }
+        if (fin) {
+            for (int q = tid; q < B * TC; q += NT) {
+                const int b = q / TC, cc = q - b * TC;
+                const int64_t col = (int64_t)tile * TC + cc;
+                if (col < A.n) {
+                    float v = s_red[b * TC + cc];
+                    if constexpr (WT == TEAL_I8) v *= A.scale[col];
+                    A.y[(int64_t)b * A.n + col] = v;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (A.kept && lane == 0 && kcount) atomicAdd(A.kept, (unsigned long long)kcount);
+}
+
+static int cpl_of(int B) { return B > 8 ? 4 : 8; }
+static int tc_of(int B) { return 32 * cpl_of(B); }
+static int bm_of(int B) { return B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : B <= 8 ? 8 : 16; }
+
+static int plan(const teal_gemv_batched_args* a, KP* P) {
+    const int tc = tc_of(a->B);
+    P->ntiles = (int)((a->n + tc - 1) / tc);
+    P->gpt = (int)((a->m + 31) / 32);
+    P->F = (int64_t)P->ntiles * P->gpt;
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        sms = 148;
+    cudaGetLastError();
+    int64_t G = a->ctas > 0 ? a->ctas : 2LL * sms;
+    if (G > P->F) G = P->F;
+    P->G = (int)G;
+    int maxc = 1;
+    for (int t = 0; t < P->ntiles; ++t) {
+        const int cf = owner_of((int64_t)t * P->gpt, P->F, P->G);
+        const int cl = owner_of((int64_t)(t + 1) * P->gpt - 1, P->F, P->G);
+        if (cl - cf + 1 > maxc) maxc = cl - cf + 1;
+    }
+    P->maxc = maxc;
+    return TEAL_OK;
+}
+
+static int validate(const teal_gemv_batched_args* a) {
+    TEAL_REQUIRE(a, "teal_gemv_batched: null args");
+    TEAL_REQUIRE(a->B >= 1 && a->B <= BMAX, "teal_gemv_batched: batch must be in [1, %d], got %d", BMAX, a->B);
+    TEAL_REQUIRE(a->m >= 1 && a->n >= 1 && a->ldw >= a->n, "teal_gemv_batched: bad shape m=%lld n=%lld ldw=%lld",
+                 (long long)a->m, (long long)a->n, (long long)a->ldw);
+    TEAL_REQUIRE(a->w_dtype == TEAL_BF16 || a->w_dtype == TEAL_I8 || a->w_dtype == TEAL_I4,
+                 "teal_gemv_batched: weights must be bf16, int8 or int4 (got %d)", a->w_dtype);
+    TEAL_REQUIRE(a->w_dtype == TEAL_BF16 || a->scale, "teal_gemv_batched: quantised weights need scales");
+    TEAL_REQUIRE(a->w_dtype != TEAL_I4 || a->group >= 1, "teal_gemv_batched: int4 needs a row-group size");
+    const int cpl = cpl_of(a->B);
+    TEAL_REQUIRE(a->n % cpl == 0 && a->ldw % cpl == 0,
+                 "teal_gemv_batched: n and ldw must be multiples of %d for batch %d", cpl, a->B);
+    TEAL_REQUIRE(a->t32 == a->t32 && (!(a->t32 < 0.f) || a->t32 == -INFINITY),
+                 "teal_gemv_batched: threshold must be >= 0 (or -inf for dense), got %g", (double)a->t32);
+    TEAL_REQUIRE(a->x && a->y && a->w, "teal_gemv_batched: null pointer");
+    return TEAL_OK;
+}
+
+template <int WT>
+static int launch_w(const KP& P, cudaStream_t st) {
+    const int bm = bm_of(P.a.B);
+    dim3 grid(P.G), block(NT);
+#define TEAL_BL(BMv, CPLv) gemv_batched_kernel<WT, BMv, CPLv><<<grid, block, 0, st>>>(P)
+    switch (bm) {
+        case 1: TEAL_BL(1, 8); break;
+        case 2: TEAL_BL(2, 8); break;
+        case 4: TEAL_BL(4, 8); break;
+        case 8: TEAL_BL(8, 8); break;
+        default: TEAL_BL(16, 4); break;
+    }
+#undef TEAL_BL
+    return check_launch("teal_gemv_batched");
+}
+
+}  // namespace batched
+}  // namespace teal
+
+using namespace teal;
+using namespace teal::batched;
+
+extern "C" {
+
+int teal_gemv_batched_workspace(const teal_gemv_batched_args* a, int* ctas, int64_t* ws_floats, int64_t* tickets) {
+    int st = validate(a);
+    if (st) return st;
+    KP P;
+    memset(&P, 0, sizeof(P));
+    plan(a, &P);
+    if (ctas) *ctas = P.G;
+    if (ws_floats) *ws_floats = (int64_t)P.ntiles * P.maxc * bm_of(a->B) * tc_of(a->B);
+    if (tickets) *tickets = P.ntiles;
+    return TEAL_OK;
+}
+
+int teal_gemv_batched(const teal_gemv_batched_args* a, cudaStream_t stream) {
+    int st = validate(a);
+    if (st) return st;
+    KP P;
+    memset(&P, 0, sizeof(P));
+    P.a = *a;
+    plan(a, &P);
+    TEAL_REQUIRE(P.G == 1 || P.maxc == 1 || (a->ws && a->tickets), "teal_gemv_batched: ws and tickets are required");
+    if (a->w_dtype == TEAL_BF16) return launch_w<TEAL_BF16>(P, stream);
+    if (a->w_dtype == TEAL_I8) return launch_w<TEAL_I8>(P, stream);
+    return launch_w<TEAL_I4>(P, stream);
+}
+
+}  // extern "C"

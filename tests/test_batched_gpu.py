@@ -1,0 +1,98 @@
+"""GPU: batched shared-mask sparse GEMV over bf16 / int8 / int4 rows
+(BASELINE config 5; quant.sparse_gemv_batched -> teal_gemv_batched).
+
+Pinned to the reference's `sparsify_batched` (sparsifier.py:136-155): the
+shared column mask is bit-exact against the oracle and the golden batched
+fixtures; outputs equal the oracle's sparsify_batched(X, t) @ W_deq^T on the
+kernel's own dequantised weights within fp32 rounding (rel 1e-5; the int4 /
+int8 / bf16 values are exact fp32 numbers, only summation order differs).
+Quantisation error itself is reported, not bounded (parity unpinned for
+quantised weights).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden, rel_err
+from oracle import actsparse_ref as R
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(seed, B, m, n):
+    g = np.random.default_rng(seed)
+    return g.standard_normal((B, m), dtype=np.float32), g.standard_normal((m, n), dtype=np.float32) / np.sqrt(m)
+
+
+@pytest.mark.parametrize("kind", ["bf16", "int8", "int4"])
+@pytest.mark.parametrize("B", [1, 2, 3, 4, 8, 13, 16])
+def test_matches_oracle(kind, B):
+    from paper_2408_14690_b200 import quant as Q
+    m, n = 1024, 768
+    xs, w = _case(100 + B, B, m, n)
+    wt = torch.from_numpy(w).cuda()
+    qw = {"bf16": Q.as_bf16, "int8": Q.quantize_int8, "int4": lambda a: Q.quantize_int4(a, 128)}[kind](wt)
+    wd = qw.dequantize().cpu().numpy()
+    for t in (0.0, 0.3, 0.6745, 1.2):
+        y, mask = Q.sparse_gemv_batched(xs, t, qw, return_mask=True)
+        xs_s, mref = R.sparsify_batched(xs, t)
+        assert np.array_equal(mask, mref), (kind, B, t)
+        ref = xs_s.astype(np.float64) @ wd.astype(np.float64)
+        assert rel_err(y, ref) < 1e-5, (kind, B, t, rel_err(y, ref))
+
+
+def test_dense_and_all_pruned():
+    from paper_2408_14690_b200 import quant as Q
+    xs, w = _case(7, 4, 512, 256)
+    qw = Q.quantize_int8(torch.from_numpy(w).cuda())
+    y = Q.sparse_gemv_batched(xs, None, qw)
+    assert rel_err(y, xs.astype(np.float64) @ qw.dequantize().cpu().numpy()) < 1e-5
+    y = Q.sparse_gemv_batched(xs, 1e9, qw)
+    assert np.all(y == 0)
+
+
+def test_batch1_equals_single_row_sparsify():
+    # B = 1 shared mask == sparsify (test_acceptance.py:216-221)
+    from paper_2408_14690_b200 import quant as Q
+    xs, w = _case(9, 1, 2048, 512)
+    qw = Q.as_bf16(torch.from_numpy(w).cuda())
+    y, mask = Q.sparse_gemv_batched(xs, 0.5, qw, return_mask=True)
+    assert np.array_equal(~mask, R.keep_mask(xs[0], 0.5))
+
+
+def test_golden_batched_masks():
+    # masks of the real reference's sparsify_batched on seeds 40000+s
+    from paper_2408_14690_b200 import quant as Q
+    g = golden("sparsify")
+    for seed in range(20):
+        gg = np.random.default_rng(40_000 + seed)
+        B = 1 + seed % 7
+        xb = gg.standard_normal((B, 300), dtype=np.float32)
+        t = float(gg.uniform(0.0, 1.5))
+        qw = Q.as_bf16(torch.randn(300, 64, device="cuda"))
+        _, mask = Q.sparse_gemv_batched(xb, t, qw, return_mask=True)
+        assert np.array_equal(np.packbits(mask), g["batched_maskbits"][seed]), seed
+
+
+def test_kept_count_and_validation():
+    from paper_2408_14690_b200 import quant as Q
+    xs, w = _case(11, 2, 640, 128)
+    qw = Q.quantize_int4(torch.from_numpy(w).cuda(), 64)
+    kept = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _, mask = Q.sparse_gemv_batched(xs, 0.4, qw, return_mask=True, kept=kept)
+    assert int(kept.item()) == int((~mask).sum())
+    with pytest.raises(ValueError, match="mismatch"):
+        Q.sparse_gemv_batched(xs[:, :320], 0.4, qw)
+    with pytest.raises(ValueError, match="B <= 16"):
+        Q.sparse_gemv_batched(np.zeros((17, 640), np.float32), 0.4, qw)
+
+
+def test_quantisation_roundtrip_error_small():
+    from paper_2408_14690_b200 import quant as Q
+    w = torch.randn(1024, 512, device="cuda")
+    for q, tol in ((Q.quantize_int8(w), 0.01), (Q.quantize_int4(w, 128), 0.12)):
+        err = (q.dequantize() - w).norm() / w.norm()
+        assert float(err) < tol
