@@ -215,6 +215,10 @@ int teal_load_residual(const void* src, int src_dtype, const int* token, int64_t
                        float* x, float* ss_out, int tile, int* step_state,
                        cudaStream_t stream);
 
+/* Tensor-parallel row-parallel epilogue after the all-reduce of the partial
+ * projections: x += delta; ss_out[t] = sum of x^2 over tile t (model.py:184,198). */
+int teal_residual_add(float* x, const float* delta, int64_t d, float* ss_out, int tile, cudaStream_t stream);
+
 /* out_token = argmax(logits) (lowest index on ties, NaN ignored). */
 int teal_argmax(const float* logits, int64_t n, int* out_token,
                 float* ws, uint32_t* tickets, cudaStream_t stream);

@@ -150,6 +150,22 @@ __global__ void __launch_bounds__(kThreads) load_residual_kernel(const ST* __res
     if (threadIdx.x == 0 && ss_out) ss_out[blockIdx.x] = s;
 }
 
+// x += delta (fp32); ss_out[t] = sum of x^2 over columns [t*tile, (t+1)*tile).
+__global__ void __launch_bounds__(kThreads) residual_add_kernel(float* __restrict__ x, const float* __restrict__ delta,
+                                                                int64_t d, float* __restrict__ ss_out, int tile) {
+    __shared__ float s_scr[kWarps + 1];
+    const int64_t c0 = (int64_t)blockIdx.x * tile;
+    const int64_t c1 = min64(d, c0 + tile);
+    float sq = 0.f;
+    for (int64_t c = c0 + threadIdx.x; c < c1; c += kThreads) {
+        const float v = x[c] + delta[c];
+        x[c] = v;
+        sq += v * v;
+    }
+    const float s = block_sum(sq, s_scr);
+    if (threadIdx.x == 0 && ss_out) ss_out[blockIdx.x] = s;
+}
+
 __device__ __forceinline__ void argmax_merge(float& bv, long long& bi, float v, long long i) {
     if (v != v) return;  // NaN ignored
     if (bi < 0 || v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
@@ -233,6 +249,13 @@ int teal_load_residual(const void* src, int src_dtype, const int* token, int64_t
     else
         TEAL_REQUIRE(false, "teal_load_residual: unsupported dtype %d", src_dtype);
     return check_launch("teal_load_residual");
+}
+
+int teal_residual_add(float* x, const float* delta, int64_t d, float* ss_out, int tile, cudaStream_t stream) {
+    TEAL_REQUIRE(x && delta && d >= 1 && tile >= 1, "teal_residual_add: bad arguments");
+    const int grid = (int)((d + tile - 1) / tile);
+    residual_add_kernel<<<grid, kThreads, 0, stream>>>(x, delta, d, ss_out, tile);
+    return check_launch("teal_residual_add");
 }
 
 int teal_argmax(const float* logits, int64_t n, int* out_token, float* ws, uint32_t* tickets, cudaStream_t stream) {

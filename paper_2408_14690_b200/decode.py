@@ -48,10 +48,11 @@ class DecoderSpec:
     rope_theta: float | None = None  # None: no positional encoding (the reference toy block)
     norm_eps: float = 1e-6         # model.py:36
     max_seq: int = 2048
+    head_dim_: int = 0             # 0: d_model // n_heads (set for tensor-parallel shards)
 
     @property
     def head_dim(self) -> int:
-        return self.d_model // self.n_heads
+        return self.head_dim_ or self.d_model // self.n_heads
 
     @property
     def n_q(self) -> int:

@@ -1,0 +1,181 @@
+"""Tensor-parallel TEAL decode (BASELINE config 4: Llama-3-70B over 2/4/8
+GPUs of one NVLink/NVSwitch box).  The reference has no
+distributed code (SPEC.md:8 puts TP out of its scope); the
+split follows the paper's setup and Megatron-style sharding:
+
+* column-parallel — q, k, v (whole heads per rank; GQA: KVH / tp kv heads per
+  rank) and gate, up (d_ff / tp columns).  Their input is the replicated
+  residual stream, so every rank computes the SAME keep mask locally; no
+  communication is needed for masks.
+* row-parallel — o (its rank's attention heads' context channels) and down
+  (its rank's d_ff intermediate channels).  Their inputs are rank-local, so
+  each rank thresholds its own channels: the global mask is the
+  concatenation of the local ones, elementwise identical to the single-GPU
+  mask.  Each produces a partial d-vector -> ALL-REDUCE(sum) -> residual add
+  + sum of squares (``teal_residual_add``).
+* LM head: column-parallel over the vocabulary; the per-rank logits are
+  all-gathered and every rank takes the same argmax.
+
+So one decode step has 2 all-reduces per layer (d fp32 each) and one
+all-gather.  The collectives are pluggable: :func:`run_step_dist` drives
+``torch.distributed`` (NCCL over NVLink; stream-ordered), and
+:func:`run_lockstep` plays all ranks on one device with an explicit
+in-order sum — the same arithmetic (rank-order fp32 sum), used to test the
+sharded kernels without a multi-GPU box.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import replace
+
+import torch
+
+from . import _clib as C
+from . import _runtime as RT
+from .decode import DecoderSpec, DecoderWeights, LayerWeights, SparseDecoder
+
+
+def shard_spec(spec: DecoderSpec, world: int) -> DecoderSpec:
+    """Per-rank shape: H/tp q heads, KVH/tp kv heads, d_ff/tp, vocab/tp."""
+    if spec.n_heads % world or spec.n_kv_heads % world or spec.d_ff % world or (spec.vocab and spec.vocab % world):
+        raise ValueError(f"tensor parallel degree {world} must divide heads {spec.n_heads}, kv heads "
+                         f"{spec.n_kv_heads}, d_ff {spec.d_ff} and vocab {spec.vocab}")
+    return replace(spec, n_heads=spec.n_heads // world, n_kv_heads=spec.n_kv_heads // world,
+                   d_ff=spec.d_ff // world, vocab=spec.vocab // world if spec.vocab else 0,
+                   head_dim_=spec.head_dim)
+
+
+def shard_weights(W: DecoderWeights, rank: int, world: int) -> DecoderWeights:
+    """Rank `rank`'s slice of input-major weights (see module docstring)."""
+    spec = W.spec
+    ls = shard_spec(spec, world)
+    nq, nkv, f = spec.n_q, spec.n_kv, spec.d_ff
+    nql, nkvl, fl = ls.n_q, ls.n_kv, ls.d_ff
+    layers = []
+    for lw in W.layers:
+        q = lw.wqkv[:, rank * nql:(rank + 1) * nql]
+        k = lw.wqkv[:, nq + rank * nkvl: nq + (rank + 1) * nkvl]
+        v = lw.wqkv[:, nq + nkv + rank * nkvl: nq + nkv + (rank + 1) * nkvl]
+        g = lw.wgu[:, rank * fl:(rank + 1) * fl]
+        u = lw.wgu[:, f + rank * fl: f + (rank + 1) * fl]
+        layers.append(LayerWeights(
+            wqkv=torch.cat([q, k, v], dim=1).contiguous(),
+            wo=lw.wo[rank * nql:(rank + 1) * nql].contiguous(),
+            wgu=torch.cat([g, u], dim=1).contiguous(),
+            wdown=lw.wdown[rank * fl:(rank + 1) * fl].contiguous(),
+            rms_attn=lw.rms_attn, rms_mlp=lw.rms_mlp))
+    head = None
+    if W.lm_head is not None:
+        vl = ls.vocab
+        head = W.lm_head[:, rank * vl:(rank + 1) * vl].contiguous()
+    return DecoderWeights(ls, layers, W.embedding, W.final_norm, head)
+
+
+class TPDecoder(SparseDecoder):
+    """One rank of a tensor-parallel decode.  `weights` are this rank's shard
+    (:func:`shard_weights`); thresholds are the model's per-layer lists (the
+    same on every rank).  Use :func:`run_step_dist` / :func:`run_lockstep`
+    to drive steps; the residual stream ``x`` and the argmax ``token`` end
+    up identical on every rank."""
+
+    def __init__(self, weights: DecoderWeights, thresholds=None, rank: int = 0, world: int = 1,
+                 full_vocab: int = 0, **kw):
+        self.rank, self.world = rank, world
+        self.full_vocab = full_vocab or weights.spec.vocab * world
+        super().__init__(weights, thresholds, **kw)
+
+    def _build(self, thresholds):
+        super()._build(thresholds)
+        d = self.spec.d_model
+        self.part = torch.zeros(d, device=self.device)
+        for (_, o, _, dn) in self.layer_args:
+            for a in (o, dn):  # row-parallel: partial projection, reduced across ranks
+                a.epilogue = C.EPI_STORE
+                a.seg[0].y = self.part.data_ptr()
+                a.resid = None
+                a.ss_out = None
+        if self.lm_args is not None:
+            self.logits_full = torch.zeros(self.full_vocab, device=self.device)
+
+    def launches_per_step(self) -> int:
+        return 1 + 7 * self.spec.n_layers + (2 if self.lm_args is not None else 0)
+
+    def step_ops(self, stream_h: int, from_token: bool):
+        """Generator over one decode step: launches this rank's kernels on
+        `stream_h` and yields ('allreduce', tensor) / ('allgather', out, in)
+        at every collective point; the driver performs the collective
+        (stream-ordered) before resuming."""
+        L = C.lib()
+        spec = self.spec
+        if from_token:
+            src, sdt, tok = self.w.embedding.data_ptr(), RT.dtype_code(self.w.embedding.dtype), self.token.data_ptr()
+        else:
+            src, sdt, tok = self.x_in.data_ptr(), C.TEAL_F32, None
+        C.check(L.teal_load_residual(src, sdt, tok, spec.d_model, self.x.data_ptr(), self.ss.data_ptr(),
+                                     self.res_tile, self.state.data_ptr(), stream_h))
+        len_ptr = self.state.data_ptr() + 4
+        for l, (qkv, o, gu, dn) in enumerate(self.layer_args):
+            C.check(L.teal_fused_gemv(ctypes.byref(qkv), stream_h))
+            C.check(L.teal_decode_attention(self.q.data_ptr(), self.kcache[l].data_ptr(), self.vcache[l].data_ptr(),
+                                            RT.dtype_code(self.kv_dtype), spec.n_heads, spec.n_kv_heads,
+                                            spec.head_dim, spec.max_seq, len_ptr, spec.max_seq,
+                                            self.ctx.data_ptr(), self.ws.data_ptr(), self.tickets.data_ptr(),
+                                            self.attn_nsplit, stream_h))
+            for args, nxt in ((o, gu), (dn, None)):
+                C.check(L.teal_fused_gemv(ctypes.byref(args), stream_h))
+                yield ("allreduce", self.part)
+                C.check(L.teal_residual_add(self.x.data_ptr(), self.part.data_ptr(), spec.d_model,
+                                            self.ss.data_ptr(), self.res_tile, stream_h))
+                if nxt is not None:
+                    C.check(L.teal_fused_gemv(ctypes.byref(nxt), stream_h))
+        if self.lm_args is not None:
+            C.check(L.teal_fused_gemv(ctypes.byref(self.lm_args), stream_h))
+            yield ("allgather", self.logits_full, self.logits[: spec.vocab])
+            C.check(L.teal_argmax(self.logits_full.data_ptr(), self.full_vocab, self.token.data_ptr(),
+                                  self.ws.data_ptr(), self.tickets.data_ptr(), stream_h))
+
+    # the single-rank entry points run the generator with an in-place driver
+    def _launch_step(self, stream_h: int, from_token: bool) -> None:
+        if self.world != 1:
+            raise RuntimeError("TPDecoder with world > 1: drive steps with run_step_dist or run_lockstep")
+        run_lockstep([self], from_token, stream_h)
+
+
+def run_step_dist(dec: TPDecoder, from_token: bool = True, group=None) -> None:
+    """One step on this rank with torch.distributed collectives (NCCL)."""
+    import torch.distributed as dist
+    for op in dec.step_ops(RT.stream_handle(), from_token):
+        if op[0] == "allreduce":
+            dist.all_reduce(op[1], group=group)
+        else:
+            dist.all_gather_into_tensor(op[1], op[2].contiguous(), group=group)
+
+
+def run_lockstep(decs, from_token: bool = True, stream_h: int | None = None) -> None:
+    """All ranks of a TP group on one device, advanced in lockstep; the
+    all-reduce sums the ranks' partials in rank order (fp32) and the
+    all-gather concatenates the vocabulary shards."""
+    sh = RT.stream_handle() if stream_h is None else stream_h
+    gens = [d.step_ops(sh, from_token) for d in decs]
+    while True:
+        ops = []
+        for g in gens:
+            try:
+                ops.append(next(g))
+            except StopIteration:
+                ops.append(None)
+        if all(o is None for o in ops):
+            return
+        if any(o is None for o in ops):
+            raise RuntimeError("tensor-parallel ranks diverged")
+        if ops[0][0] == "allreduce":
+            total = ops[0][1].clone()
+            for o in ops[1:]:
+                total += o[1]
+            for o in ops:
+                o[1].copy_(total)
+        else:
+            full = torch.cat([o[2] for o in ops])
+            for o in ops:
+                o[1].copy_(full)
