@@ -94,7 +94,7 @@ __device__ __forceinline__ void wait_range(const int* counters, int c0, int c1, 
             unsigned ns = 32;
             while (ld_acquire(counters + (int64_t)c * CSTRIDE) < target) {
                 __nanosleep(ns);
-                ns = ns < 512 ? ns * 2 : 512;
+                ns = ns < 128 ? ns * 2 : 128;
             }
         }
     }
@@ -293,6 +293,18 @@ __device__ __forceinline__ float rms_den(const teal_step_group& g, int lane) {
     return sqrtf(a / (float)g.m + g.eps);
 }
 
+// CTAs taking part in a GEMV phase: never more than the 32-row groups (every
+// range non-empty) and, when the phase has at most half as many tiles as the
+// grid has CTAs, a multiple of the tile count so that every range lies inside
+// one tile (no CTA pays the fixed cost of a second segment; each tile has the
+// same number of contributors).  Mirrored by engine.participants().
+__device__ __forceinline__ int participants(int ntiles, int64_t F) {
+    const int grid = gridDim.x;
+    if (F <= grid) return (int)F;
+    if (2 * ntiles <= grid) return ntiles * (grid / ntiles);
+    return grid;
+}
+
 __device__ __forceinline__ int owner_of(int64_t gidx, int64_t F, int G) {
     return (int)(((gidx + 1) * (int64_t)G - 1) / F);
 }
@@ -445,7 +457,7 @@ __device__ void gemv_slice(const teal_step_plan& P, const teal_step_phase& ph, S
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gpt = (g.m + 31) / 32;
     const int64_t F = (int64_t)g.ntiles * gpt;
-    const int G = (int)min64((int64_t)gridDim.x, F), c = blockIdx.x;  // every participating range is non-empty
+    const int G = participants(g.ntiles, F), c = blockIdx.x;
     if (c >= G) return;
     const int64_t g0 = (int64_t)c * F / G, g1 = (int64_t)(c + 1) * F / G;
     const bool rms = g.prologue == TEAL_PRO_RMSNORM;
@@ -545,13 +557,19 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
         const uint4* gv = reinterpret_cast<const uint4*>(reinterpret_cast<const KT*>(a.v_cache) + kvbase + (int64_t)p0 * hd);
         for (int o = tid; o < G * hd; o += NT) s.u.a.q[o] = __ldcg(a.q + (int64_t)g * G * hd + o);
 #pragma unroll 1
-        for (int v = tid; v < n16; v += 2 * NT) {
-            const uint4 k0 = __ldcg(gk + v), v0 = __ldcg(gv + v);
-            uint4 k1 = make_uint4(0u, 0u, 0u, 0u), v1 = k1;
-            if (v + NT < n16) { k1 = __ldcg(gk + v + NT); v1 = __ldcg(gv + v + NT); }
-            s.u.a.k[v] = k0;
-            s.u.a.v[v] = v0;
-            if (v + NT < n16) { s.u.a.k[v + NT] = k1; s.u.a.v[v + NT] = v1; }
+        {  // n16 <= ATT_STAGE / 16 = 4 * NT: every thread's loads in flight together
+            constexpr int PER = ATT_STAGE / 16 / NT;
+            uint4 kk[PER], vv[PER];
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int v = tid + q * NT;
+                if (v < n16) { kk[q] = __ldcg(gk + v); vv[q] = __ldcg(gv + v); }
+            }
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int v = tid + q * NT;
+                if (v < n16) { s.u.a.k[v] = kk[q]; s.u.a.v[v] = vv[q]; }
+            }
         }
         __syncthreads();
         const KT* ks = reinterpret_cast<const KT*>(s.u.a.k);
@@ -592,7 +610,10 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
             if (lane == 0) { s.am[h] = mx; s.al[h] = l; }
         }
         __syncthreads();
-        // context partial: thread -> (head, d), positions ascending
+        // context partial: thread -> (head, d), positions ascending.  A
+        // single chunk holding every position is final: normalise and write
+        // the context directly (no partial record, ticket or combine).
+        const bool single = (p0 == 0 && p1 == L);
 #pragma unroll 1
         for (int o = tid; o < G * hd; o += NT) {
             const int h = o / hd, d = o - h * hd;
@@ -600,7 +621,14 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
             float acc = 0.f;
 #pragma unroll 4
             for (int p = 0; p < np; ++p) acc = fmaf(pr[p], to_f32<KT>(vs[p * hd + d]), acc);
-            __stcg(my + o, acc);
+            if (single) a.ctx[(int64_t)g * G * hd + o] = acc / s.al[h];
+            else __stcg(my + o, acc);
+        }
+        if (single) {
+            ATT_STAMP(4);
+            signal(P.counters, a.sig_base + g, a.sig_base + g);
+            ATT_STAMP(5);
+            return;
         }
         if (tid < G) {
             __stcg(my + G * hd + tid, s.am[tid]);
@@ -611,7 +639,9 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
         __stcg(my + G * hd + G + tid, 0.f);
     }
     ATT_STAMP(2);
-    const bool last = take_ticket(a.tickets + g, (unsigned)a.nchunks - 1u, s.last);
+    // only the chunks holding positions take part (the attn phase skips the rest)
+    const int nact_t = min(a.nchunks, (L + a.chunk - 1) / a.chunk);
+    const bool last = take_ticket(a.tickets + g, (unsigned)nact_t - 1u, s.last);
     ATT_STAMP(3);
     if (!last) return;
     const float* rb = a.partials + (int64_t)g * a.nchunks * rec;
@@ -656,11 +686,18 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
 
 __device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, Smem& s) {
     const teal_step_attn& a = P.attns[ph.group];
-    const int nu = a.KVH * a.nchunks;
+    // the sequence length is written by this step's load phase: a CTA that had
+    // no qkv slice reaches this point without having waited for it
+    wait_range(P.counters, 0, 0, 1);
+    const int L = __ldcg(P.state + 1);
+    const int nact = min(a.nchunks, (L + a.chunk - 1) / a.chunk);  // chunks holding positions
+    const int nu = a.KVH * nact;
     const int G = gridDim.x;
-    // unit u runs on CTA (u * G) / nu: spread over the grid (different SMs)
-    for (int u = (int)(((int64_t)blockIdx.x * nu + G - 1) / G); u < nu && (int64_t)u * G / nu == blockIdx.x; ++u) {
-        const int g = u / a.nchunks, ch = u % a.nchunks;
+    // unit u = (chunk u / KVH, kv group u % KVH) runs on CTA G-1 - (u*G)/nu:
+    // spread over the grid from its end (the qkv phase leaves the last CTAs idle)
+    const int cr = G - 1 - (int)blockIdx.x;
+    for (int u = (int)(((int64_t)cr * nu + G - 1) / G); u < nu && (int64_t)u * G / nu == cr; ++u) {
+        const int g = u % a.KVH, ch = u / a.KVH;
         wait_range(P.counters, a.dep_base + g, a.dep_base + g, a.dep_target[g]);
         if (a.kv_dtype == TEAL_BF16) attn_unit_t<uint16_t>(P, a, g, ch, s);
         else attn_unit_t<float>(P, a, g, ch, s);

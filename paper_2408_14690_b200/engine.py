@@ -71,12 +71,21 @@ PHASE_LOAD, PHASE_GEMV, PHASE_ATTN = 0, 1, 2
 DEP_NONE, DEP_GLOBAL, DEP_ROWS = 0, 1, 2
 
 
+def participants(ntiles: int, F: int, grid: int) -> int:
+    """CTAs taking part in a GEMV phase (csrc/teal_step.cu participants())."""
+    if F <= grid:
+        return F
+    if 2 * ntiles <= grid:
+        return ntiles * (grid // ntiles)
+    return grid
+
+
 def max_contributors(ntiles: int, m: int, G: int) -> int:
     """Most CTAs sharing one tile under the equal-range split of the
     flattened (tile, 32-row group) space (csrc/teal_step.cu owner_of)."""
     gpt = -(-m // 32)
     F = ntiles * gpt
-    G = min(G, F)
+    G = participants(ntiles, F, G)
 
     def owner(x):
         return ((x + 1) * G - 1) // F

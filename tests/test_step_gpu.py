@@ -45,6 +45,18 @@ def test_toy_dense_rows_match_reference(toy):
     assert max(errs) < 1e-5, max(errs)
 
 
+@pytest.mark.parametrize("chunk", [8, 32, 64])
+def test_toy_attention_chunking(toy, chunk):
+    # single-chunk fast path, multi-chunk combine, and CTAs that reach the
+    # attention phase without a qkv slice (they must wait for the step's load)
+    D, E, _, W = toy
+    g = golden("toy_model")
+    dec = E.StepDecoder(W, _thr(g), attn_chunk=chunk)
+    dec.reset()
+    errs = [rel_err(dec.step_hidden(g["X"][t]).cpu().numpy(), g["out_sparse50"][t]) for t in range(40)]
+    assert np.median(errs) < 1e-5 and max(errs) < 1e-4, (chunk, np.median(errs), max(errs))
+
+
 def test_toy_sparse50_rows_match_reference(toy):
     D, E, _, W = toy
     g = golden("toy_model")
