@@ -251,17 +251,37 @@ __device__ __noinline__ void finalize(const teal_step_plan& P, const teal_step_g
                 P.cand_i[tile] = ti;
                 __threadfence();
                 const unsigned prev = atomicAdd(P.lm_done, 1u);
-                if (prev == (unsigned)g.ntiles - 1u) {
+                s.last = prev == (unsigned)g.ntiles - 1u;
+                if (s.last) {
                     *P.lm_done = 0u;
                     __threadfence();
-                    float gv = -INFINITY;
-                    int gi = 0x7fffffff;
-                    for (int t = 0; t < g.ntiles; ++t) {
-                        const float cv = __ldcg(P.cand_v + t);
-                        const int ci = __ldcg(P.cand_i + t);
-                        if (cv > gv || (cv == gv && ci < gi)) { gv = cv; gi = ci; }
-                    }
-                    *P.token_out = gi == 0x7fffffff ? 0 : gi;
+                }
+            }
+            __syncthreads();
+            if (s.last) {  // the last tile: argmax over the per-tile candidates, whole CTA
+                float gv = -INFINITY;
+                int gi = 0x7fffffff;
+                for (int t = c; t < g.ntiles; t += NT) {
+                    const float cv = __ldcg(P.cand_v + t);
+                    const int ci = __ldcg(P.cand_i + t);
+                    if (cv > gv || (cv == gv && ci < gi)) { gv = cv; gi = ci; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float ov = __shfl_xor_sync(0xffffffffu, gv, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, gi, o);
+                    if (ov > gv || (ov == gv && oi < gi)) { gv = ov; gi = oi; }
+                }
+                __syncthreads();
+                if ((c & 31) == 0) { s.scr[c >> 5] = gv; s.wcnt[c >> 5] = gi; }
+                __syncthreads();
+                if (c == 0) {
+                    for (int w = 1; w < NW; ++w)
+                        if (s.scr[w] > s.scr[0] || (s.scr[w] == s.scr[0] && s.wcnt[w] < s.wcnt[0])) {
+                            s.scr[0] = s.scr[w];
+                            s.wcnt[0] = s.wcnt[w];
+                        }
+                    *P.token_out = s.wcnt[0] == 0x7fffffff ? 0 : s.wcnt[0];
                 }
             }
             __syncthreads();
