@@ -295,7 +295,10 @@ typedef struct teal_step_group {
     float eps;
     int epilogue;
     int nq, nkv, head_dim, kv_dtype;
-    int pad_;
+    int w_dtype;             /* TEAL_F32 / TEAL_BF16 / TEAL_I8 (col_scale) / TEAL_I4 (gscale) */
+    const float* gscale;     /* TEAL_I4: [ceil(m/group)][ntiles*TW] fp32      */
+    int group;               /* TEAL_I4 row-group size (>= 128)              */
+    int pad2_;
 } teal_step_group;
 
 typedef struct teal_step_attn {
@@ -337,8 +340,10 @@ typedef struct teal_step_plan {
     int* cand_i;
     int* token_out;                  /* LOGITS: argmax token                   */
     unsigned* lm_done;               /* LOGITS: tiles finished (self-resetting) */
-    unsigned long long* timeline;    /* nullable debug: [ctas][nphases][2] %globaltimer */
+    unsigned long long* timeline;    /* nullable debug: [ctas][nphases][8] %globaltimer */
     int nphases, ncounters;
+    int prefetch_bytes;              /* per CTA per GEMV phase: L2 prefetch of its weight range head (0: off) */
+    int pad_;
     int d, emb_dtype;
     int w_dtype, ctas;               /* ctas: grid size (<= resident capacity)  */
 } teal_step_plan;

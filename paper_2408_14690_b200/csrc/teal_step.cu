@@ -48,6 +48,7 @@ constexpr int TH = TW / 2;        // columns per half
 constexpr int NT = 256;           // threads per CTA (== TW: one column per thread in epilogues)
 constexpr int NW = NT / 32;
 constexpr int MAXR = 1024;        // rows per compaction chunk
+constexpr int GSC_MAX = 9;        // int4 row groups one chunk can touch (group >= 128)
 constexpr int ATT_MAXG = 8;
 constexpr int ATT_MAXHD = 128;
 constexpr int ATT_MAXCHUNK = 256;
@@ -59,6 +60,7 @@ struct Smem {
         struct {
             int idx[MAXR];    // row - r0 | keep_lo << 30 | keep_hi << 31
             float h[MAXR];
+            float gsc[GSC_MAX * TW];  // int4: scales of the chunk's row groups
         } g;
         struct {
             float q[ATT_MAXG * ATT_MAXHD];
@@ -293,12 +295,60 @@ __device__ __noinline__ void finalize(const teal_step_plan& P, const teal_step_g
     signal(P.counters, tm.sig0, tm.sig1);
 }
 
-// Per-lane accumulator columns: bf16 lane l owns [8l, 8l+8) (lanes 16..31 =
-// hi half); fp32 lane l owns [4l, 4l+4) (lo) and [128+4l, 128+4l+4) (hi).
-template <int ESZ>
+// Weight element formats of a tile row chunk (TW columns):
+//   fp32 1 KB, bf16 512 B, int8 256 B (per-column scale applied after the
+//   reduction), int4 128 B (two's-complement nibbles, low nibble = even
+//   column; fp32 scale per (row group, column)).
+// Per-lane accumulator columns: bf16 / int8 / int4 lane l owns [8l, 8l+8)
+// (lanes 16..31 = hi half); fp32 lane l owns [4l, 4l+4) (lo) and
+// [128+4l, 128+4l+4) (hi).
+template <int WT> struct WFmt;
+template <> struct WFmt<TEAL_F32> { static constexpr int ROWB = TW * 4; static constexpr int LB = 16; };
+template <> struct WFmt<TEAL_BF16> { static constexpr int ROWB = TW * 2; static constexpr int LB = 16; };
+template <> struct WFmt<TEAL_I8> { static constexpr int ROWB = TW; static constexpr int LB = 8; };
+template <> struct WFmt<TEAL_I4> { static constexpr int ROWB = TW / 2; static constexpr int LB = 4; };
+
+template <int WT>
 __device__ __forceinline__ int acc_col(int lane, int j) {
-    if constexpr (ESZ == 2) return lane * 8 + j;
+    if constexpr (WT != TEAL_F32) return lane * 8 + j;
     else return j < 4 ? lane * 4 + j : TH + lane * 4 + (j - 4);
+}
+
+// one lane's raw weights of a row chunk: 8 words (fp32), 4 (bf16), 2 (int8), 1 (int4)
+template <int WT> struct LaneW { static constexpr int N = WT == TEAL_F32 ? 8 : (WT == TEAL_BF16 ? 4 : (WT == TEAL_I8 ? 2 : 1)); uint32_t u[N]; };
+
+// lane's 8 weights of one row chunk (unscaled for int8 / int4)
+template <int WT>
+__device__ __forceinline__ void unpack8(const LaneW<WT>& d, float w[8]) {
+    if constexpr (WT == TEAL_BF16) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { w[2 * q] = bf16_lo(d.u[q]); w[2 * q + 1] = bf16_hi(d.u[q]); }
+    } else if constexpr (WT == TEAL_F32) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w[q] = __uint_as_float(d.u[q]);
+    } else if constexpr (WT == TEAL_I8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = (float)(int8_t)((d.u[k >> 2] >> (8 * (k & 3))) & 0xffu);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int nib = (int)((d.u[0] >> (4 * k)) & 0xfu);
+            w[k] = (float)(nib >= 8 ? nib - 16 : nib);
+        }
+    }
+}
+
+// streaming load of 16 / 8 / 4 bytes (L2 evict-first policy), by value
+__device__ __forceinline__ uint4 ldw16(const unsigned char* p, uint64_t pol) { return ldg128_stream_pol(p, pol); }
+__device__ __forceinline__ uint2 ldw8(const unsigned char* p, uint64_t pol) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint32_t ldw4(const unsigned char* p, uint64_t pol) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
 }
 
 // sqrt(sum(ss)/m + eps) with the partials summed in ascending order: one
@@ -394,86 +444,123 @@ __device__ int compact_rows(const teal_step_group& g, const teal_step_tile& tm, 
 }
 
 // Stream the `cnt` compacted rows: warp w takes rows w*U.., w*U+NW*U.., with
-// the next batch of U rows' 16-byte loads issued before the current batch is
-// consumed (software pipeline: 2U row chunks in flight per warp).  Only the
-// kept half of a row is loaded (bf16: lanes 0-15 = lo, 16-31 = hi; fp32:
-// every lane loads 16 B of each kept half).
-template <int ESZ, int UB>
+// the next batch of U rows' loads issued before the current batch is consumed
+// (software pipeline: 2U row chunks in flight per warp).  Only the kept half
+// of a row is loaded (bf16 / int8 / int4: lanes 0-15 = lo, 16-31 = hi; fp32:
+// every lane loads 16 B of each kept half).  int4 rows accumulate per row
+// group and are scaled when the group changes (scales staged in s.u.g.gsc).
+template <int WT, int UB>
 __device__ __forceinline__ void stream_rows(const unsigned char* tb, int cnt, const Smem& s, float acc[8],
-                                            uint64_t pol) {
-    constexpr int ROWB = TW * ESZ;
+                                            uint64_t pol, int gbase, int group) {
+    constexpr int ROWB = WFmt<WT>::ROWB;
+    constexpr int LB = WFmt<WT>::LB;
     constexpr int HB = ROWB / 2;
-    constexpr int U = ESZ == 2 ? UB : UB / 2;
-    constexpr int NV = ESZ == 2 ? 1 : 2;  // 16-byte vectors per lane per row
+    // rows per pipeline stage: equal bytes in flight for every format (UB bf16 rows)
+    constexpr int U = WT == TEAL_F32 ? UB / 2 : (WT == TEAL_BF16 ? UB : (WT == TEAL_I8 ? 2 * UB : 4 * UB));
+    constexpr int NW_ = LaneW<WT>::N;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint4 a[U][NV], b[U][NV];
-    float ha[U][NV], hb[U][NV];
-    auto fetch = [&](int e0, uint4 (&d)[U][NV], float (&hh)[U][NV]) {
+    const int myhalf = lane < 16 ? 30 : 31;
+    LaneW<WT> a[U], b[U];
+    float accg[8];
+    int curg = -1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) accg[j] = 0.f;
+    // loads only: the kept bits and h are re-read from shared memory when consumed
+    auto fetch = [&](int e0, LaneW<WT> (&d)[U]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int e = e0 + u;
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                d[u][v] = make_uint4(0u, 0u, 0u, 0u);
-                hh[u][v] = 0.f;
-            }
+            for (int k = 0; k < NW_; ++k) d[u].u[k] = 0u;
             if (e < cnt) {
                 const unsigned pk = (unsigned)s.u.g.idx[e];
-                const float h = s.u.g.h[e];
-                const unsigned char* row = tb + (int64_t)(pk & 0x3fffffffu) * ROWB + lane * 16;
-                if constexpr (ESZ == 2) {
-                    if ((pk >> (lane < 16 ? 30 : 31)) & 1u) {
-                        d[u][0] = ldg128_stream_pol(row, pol);
-                        hh[u][0] = h;
+                const unsigned char* rp = tb + (int64_t)(pk & 0x3fffffffu) * ROWB;
+                if constexpr (WT == TEAL_F32) {
+                    if ((pk >> 30) & 1u) {
+                        const uint4 r = ldw16(rp + lane * 16, pol);
+                        d[u].u[0] = r.x; d[u].u[1] = r.y; d[u].u[2] = r.z; d[u].u[3] = r.w;
                     }
-                } else {
-                    if ((pk >> 30) & 1u) { d[u][0] = ldg128_stream_pol(row, pol); hh[u][0] = h; }
-                    if ((pk >> 31) & 1u) { d[u][NV - 1] = ldg128_stream_pol(row + HB, pol); hh[u][NV - 1] = h; }
+                    if ((pk >> 31) & 1u) {
+                        const uint4 r = ldw16(rp + HB + lane * 16, pol);
+                        d[u].u[4] = r.x; d[u].u[5] = r.y; d[u].u[6] = r.z; d[u].u[7] = r.w;
+                    }
+                } else if ((pk >> myhalf) & 1u) {
+                    if constexpr (LB == 16) {
+                        const uint4 r = ldw16(rp + lane * 16, pol);
+                        d[u].u[0] = r.x; d[u].u[1] = r.y; d[u].u[2] = r.z; d[u].u[3] = r.w;
+                    } else if constexpr (LB == 8) {
+                        const uint2 r = ldw8(rp + lane * 8, pol);
+                        d[u].u[0] = r.x; d[u].u[1] = r.y;
+                    } else {
+                        d[u].u[0] = ldw4(rp + lane * 4, pol);
+                    }
                 }
             }
         }
     };
-    auto consume = [&](const uint4 (&d)[U][NV], const float (&hh)[U][NV]) {
+    auto flush_group = [&]() {  // int4: acc += accg * scale(group, column)
+        if (curg >= 0) {
+            const float* sc = s.u.g.gsc + (curg - gbase / group) * TW + lane * 8;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                acc[j] = fmaf(accg[j], sc[j], acc[j]);
+                accg[j] = 0.f;
+            }
+        }
+    };
+    auto consume = [&](int e0, const LaneW<WT> (&d)[U]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if constexpr (ESZ == 2) {
-                const uint32_t w4[4] = {d[u][0].x, d[u][0].y, d[u][0].z, d[u][0].w};
+            const int e = e0 + u;
+            if (e >= cnt) break;
+            const unsigned pk = (unsigned)s.u.g.idx[e];
+            const float hv = s.u.g.h[e];
+            float w[8];
+            unpack8<WT>(d[u], w);
+            if constexpr (WT == TEAL_F32) {
+                const float h0 = ((pk >> 30) & 1u) ? hv : 0.f, h1 = ((pk >> 31) & 1u) ? hv : 0.f;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    acc[2 * q] = fmaf(hh[u][0], bf16_lo(w4[q]), acc[2 * q]);
-                    acc[2 * q + 1] = fmaf(hh[u][0], bf16_hi(w4[q]), acc[2 * q + 1]);
-                }
+                for (int k = 0; k < 4; ++k) acc[k] = fmaf(h0, w[k], acc[k]);
+#pragma unroll
+                for (int k = 4; k < 8; ++k) acc[k] = fmaf(h1, w[k], acc[k]);
             } else {
+                const float h = ((pk >> myhalf) & 1u) ? hv : 0.f;
+                if constexpr (WT == TEAL_I4) {
+                    const int gr = (gbase + (int)(pk & 0x3fffffffu)) / group;
+                    if (gr != curg) {
+                        flush_group();
+                        curg = gr;
+                    }
 #pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    acc[4 * v + 0] = fmaf(hh[u][v], __uint_as_float(d[u][v].x), acc[4 * v + 0]);
-                    acc[4 * v + 1] = fmaf(hh[u][v], __uint_as_float(d[u][v].y), acc[4 * v + 1]);
-                    acc[4 * v + 2] = fmaf(hh[u][v], __uint_as_float(d[u][v].z), acc[4 * v + 2]);
-                    acc[4 * v + 3] = fmaf(hh[u][v], __uint_as_float(d[u][v].w), acc[4 * v + 3]);
+                    for (int k = 0; k < 8; ++k) accg[k] = fmaf(h, w[k], accg[k]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) acc[k] = fmaf(h, w[k], acc[k]);
                 }
             }
         }
     };
     int e0 = warp * U;
-    if (e0 >= cnt) return;
-    fetch(e0, a, ha);
-    for (;;) {
-        const int en = e0 + NW * U;
-        if (en < cnt) fetch(en, b, hb);
-        consume(a, ha);
-        if (en >= cnt) break;
-        e0 = en;
-        if (e0 + NW * U < cnt) fetch(e0 + NW * U, a, ha);
-        consume(b, hb);
-        if (e0 + NW * U >= cnt) break;
-        e0 += NW * U;
+    if (e0 < cnt) {
+        fetch(e0, a);
+        for (;;) {
+            const int en = e0 + NW * U;
+            if (en < cnt) fetch(en, b);
+            consume(e0, a);
+            if (en >= cnt) break;
+            e0 = en;
+            if (e0 + NW * U < cnt) fetch(e0 + NW * U, a);
+            consume(e0, b);
+            if (e0 + NW * U >= cnt) break;
+            e0 += NW * U;
+        }
     }
+    if constexpr (WT == TEAL_I4) flush_group();
 }
 
-template <int ESZ, int UB>
-__device__ void gemv_slice(const teal_step_plan& P, const teal_step_phase& ph, Smem& s, uint64_t pol,
-                           unsigned long long* tl) {
-    const teal_step_group& g = P.groups[ph.group];
+template <int WT, int UB>
+__device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph, const teal_step_group& g, Smem& s,
+                             uint64_t pol, unsigned long long* tl) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gpt = (g.m + 31) / 32;
     const int64_t F = (int64_t)g.ntiles * gpt;
@@ -481,6 +568,21 @@ __device__ void gemv_slice(const teal_step_plan& P, const teal_step_phase& ph, S
     if (c >= G) return;
     const int64_t g0 = (int64_t)c * F / G, g1 = (int64_t)(c + 1) * F / G;
     const bool rms = g.prologue == TEAL_PRO_RMSNORM;
+    // While this slice waits for its inputs, pull the head of its weight range
+    // into L2 (one bulk prefetch of contiguous tiled rows): the wait is tail
+    // time of the previous phase, when HBM is mostly idle.  Rows that turn out
+    // pruned cost idle bandwidth only; kept rows then stream from L2.
+    if (tid == 0 && P.prefetch_bytes > 0) {
+        const int tile = (int)(g0 / gpt);
+        const int r0 = (int)(g0 - (int64_t)tile * gpt) * 32;
+        const int r1 = min(g.m, (int)(min64(g1, (int64_t)(tile + 1) * gpt) - (int64_t)tile * gpt) * 32);
+        const int64_t rowb = WFmt<WT>::ROWB;
+        const int64_t bytes = min64((int64_t)(r1 - r0) * rowb, (int64_t)P.prefetch_bytes) & ~(int64_t)15;
+        if (bytes > 0) {
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(g.w) + ((int64_t)tile * g.m + r0) * rowb;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((uint32_t)bytes) : "memory");
+        }
+    }
     if (ph.dep_kind == TEAL_DEP_GLOBAL) wait_range(P.counters, ph.dep, ph.dep, ph.target);
     float rden = 1.f;
     if (rms) {
@@ -488,7 +590,7 @@ __device__ void gemv_slice(const teal_step_plan& P, const teal_step_phase& ph, S
         __syncthreads();
         rden = s.rden;
     }
-    constexpr int ROWB = TW * ESZ;
+    constexpr int ROWB = WFmt<WT>::ROWB;
     int segi = 0, lasts = 0;
 #define SL_STAMP(k, v) do { if (tl && tid == 0) tl[k] = (v); } while (0)
     for (int64_t gs = g0; gs < g1; ++segi) {
@@ -508,12 +610,18 @@ __device__ void gemv_slice(const teal_step_plan& P, const teal_step_phase& ph, S
         for (int ra = r0; ra < r1; ra += MAXR) {
             const int rb = min(r1, ra + MAXR);
             const int cnt = compact_rows(g, tm, tile, ra, rb, rden, rms, s);
-            stream_rows<ESZ, UB>(tbase + (int64_t)ra * ROWB, cnt, s, acc, pol);
+            if constexpr (WT == TEAL_I4) {  // stage the chunk's row-group scales (one L2 round trip)
+                const int gA = ra / g.group, gB = (rb - 1) / g.group;
+                for (int q = tid; q < (gB - gA + 1) * TW; q += NT)
+                    s.u.g.gsc[q] = __ldg(g.gscale + (int64_t)(gA + q / TW) * g.ntiles * TW + (int64_t)tile * TW + q % TW);
+                __syncthreads();
+            }
+            stream_rows<WT, UB>(tbase + (int64_t)ra * ROWB, cnt, s, acc, pol, ra, g.group > 0 ? g.group : 1);
             __syncthreads();  // rows list is rewritten by the next chunk
         }
         SL_STAMP(segi == 0 ? 3 : 5, gtimer());
 #pragma unroll
-        for (int j = 0; j < 8; ++j) s.red[warp * TW + acc_col<ESZ>(lane, j)] = acc[j];
+        for (int j = 0; j < 8; ++j) s.red[warp * TW + acc_col<WT>(lane, j)] = acc[j];
         __syncthreads();
         float v = 0.f;
 #pragma unroll
@@ -548,6 +656,9 @@ __device__ void gemv_slice(const teal_step_plan& P, const teal_step_phase& ph, S
     SL_STAMP(7, (unsigned long long)lasts);
 #undef SL_STAMP
 }
+
+// One kernel instantiation per weight format: every GEMV group of a plan
+// (layers and LM head) uses the plan's w_dtype.
 
 // ---- attention unit: (kv head g, position chunk) -------------------------------
 // Deliberately compact code (runtime loops over heads and head_dim chunks):
@@ -773,7 +884,7 @@ __device__ __noinline__ void load_phase(const teal_step_plan& P, Smem& s) {
 
 // MINB resident CTAs per SM (register budget 65536 / (NT * MINB)); UB rows in
 // flight per warp per pipeline stage.
-template <int ESZ, int MINB, int UB>
+template <int WT, int MINB, int UB>
 __global__ void __launch_bounds__(NT, MINB) step_kernel(const __grid_constant__ teal_step_plan P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
@@ -783,7 +894,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const __grid_constant__ 
         const teal_step_phase ph = P.phases[p];
         unsigned long long* tl = P.timeline ? P.timeline + ((int64_t)blockIdx.x * P.nphases + p) * 8 : nullptr;
         if (tl && tid == 0) tl[0] = gtimer();
-        if (ph.kind == TEAL_PHASE_GEMV) gemv_slice<ESZ, UB>(P, ph, s, pol, tl);
+        if (ph.kind == TEAL_PHASE_GEMV) gemv_slice_t<WT, UB>(P, ph, P.groups[ph.group], s, pol, tl);
         else if (ph.kind == TEAL_PHASE_ATTN) attn_phase(P, ph, s);
         else load_phase(P, s);
         __syncthreads();
@@ -812,26 +923,35 @@ static int occ_mode() {
     return v;
 }
 
-template <int ESZ>
-static void* kernel_ptr() {
-    if (occ_mode() == 2) return (void*)step_kernel<ESZ, 2, 8>;
-    return (void*)step_kernel<ESZ, 3, 4>;
+template <int WT>
+static void* kernel_ptr_t() {
+    if (occ_mode() == 2) return (void*)step_kernel<WT, 2, 8>;
+    return (void*)step_kernel<WT, 3, 4>;
 }
 
-template <int ESZ>
-static int occupancy() {
-    static int cached = -1;
-    if (cached < 0) {
-        const void* k = kernel_ptr<ESZ>();
+static void* kernel_ptr(int w_dtype) {
+    switch (w_dtype) {
+        case TEAL_BF16: return kernel_ptr_t<TEAL_BF16>();
+        case TEAL_I8: return kernel_ptr_t<TEAL_I8>();
+        case TEAL_I4: return kernel_ptr_t<TEAL_I4>();
+        default: return kernel_ptr_t<TEAL_F32>();
+    }
+}
+
+static int occupancy(int w_dtype) {
+    static int cached[4] = {-1, -1, -1, -1};
+    int& cache = cached[w_dtype & 3];
+    if (cache < 0) {
+        const void* k = kernel_ptr(w_dtype);
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         int b = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, NT, kSmemBytes) != cudaSuccess) {
             cudaGetLastError();
             return 0;
         }
-        cached = b;
+        cache = b;
     }
-    return cached;
+    return cache;
 }
 
 }  // namespace step
@@ -843,8 +963,7 @@ using namespace teal::step;
 extern "C" {
 
 int teal_step_ctas_per_sm(int w_dtype) {
-    if (w_dtype == TEAL_BF16) return occupancy<2>();
-    if (w_dtype == TEAL_F32) return occupancy<4>();
+    if (w_dtype == TEAL_BF16 || w_dtype == TEAL_F32 || w_dtype == TEAL_I8 || w_dtype == TEAL_I4) return occupancy(w_dtype);
     return 0;
 }
 
@@ -853,7 +972,8 @@ int teal_step_launch(const teal_step_plan* p, cudaStream_t stream) {
                  "teal_step_launch: null plan field");
     TEAL_REQUIRE(p->nphases >= 1 && p->ncounters >= 1, "teal_step_launch: empty plan");
     TEAL_REQUIRE(p->d >= TW && p->d % TW == 0, "teal_step_launch: d must be a multiple of %d", TW);
-    TEAL_REQUIRE(p->w_dtype == TEAL_BF16 || p->w_dtype == TEAL_F32, "teal_step_launch: weights must be bf16 or fp32");
+    TEAL_REQUIRE(p->w_dtype == TEAL_BF16 || p->w_dtype == TEAL_F32 || p->w_dtype == TEAL_I8 || p->w_dtype == TEAL_I4,
+                 "teal_step_launch: weights must be bf16, fp32, int8 or int4");
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -872,7 +992,7 @@ int teal_step_launch(const teal_step_plan* p, cudaStream_t stream) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     void* args[1] = {(void*)p};
-    cudaLaunchKernelExC(&cfg, p->w_dtype == TEAL_BF16 ? kernel_ptr<2>() : kernel_ptr<4>(), args);
+    cudaLaunchKernelExC(&cfg, kernel_ptr(p->w_dtype), args);
     return check_launch("teal_step_launch");
 }
 

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -46,7 +47,8 @@ class StepGroup(ctypes.Structure):
                 ("rope_sin", c_vp), ("dbg_h", c_vp), ("dbg_bits", c_vp * 3), ("kept", c_vp * 3),
                 ("max_seq", c_i64), ("m", c_i), ("n", c_i), ("ntiles", c_i), ("maxc", c_i),
                 ("prologue", c_i), ("nss", c_i), ("eps", c_f), ("epilogue", c_i),
-                ("nq", c_i), ("nkv", c_i), ("head_dim", c_i), ("kv_dtype", c_i), ("pad_", c_i)]
+                ("nq", c_i), ("nkv", c_i), ("head_dim", c_i), ("kv_dtype", c_i), ("w_dtype", c_i),
+                ("gscale", c_vp), ("group", c_i), ("pad2_", c_i)]
 
 
 class StepAttn(ctypes.Structure):
@@ -64,7 +66,8 @@ class StepPlan(ctypes.Structure):
     _fields_ = [("groups", c_vp), ("attns", c_vp), ("phases", c_vp), ("counters", c_vp), ("ctrl", c_vp),
                 ("emb", c_vp), ("x_in", c_vp), ("token", c_vp), ("x", c_vp), ("ss", c_vp), ("state", c_vp),
                 ("cand_v", c_vp), ("cand_i", c_vp), ("token_out", c_vp), ("lm_done", c_vp), ("timeline", c_vp),
-                ("nphases", c_i), ("ncounters", c_i), ("d", c_i), ("emb_dtype", c_i), ("w_dtype", c_i), ("ctas", c_i)]
+                ("nphases", c_i), ("ncounters", c_i), ("prefetch_bytes", c_i), ("pad_", c_i),
+                ("d", c_i), ("emb_dtype", c_i), ("w_dtype", c_i), ("ctas", c_i)]
 
 
 PHASE_LOAD, PHASE_GEMV, PHASE_ATTN = 0, 1, 2
@@ -134,6 +137,85 @@ def pack_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor, tw: int = TW) -> torc
     return out
 
 
+@dataclass
+class TiledW:
+    """One group's tiled weights: data [ntiles, m, TW] (fp32 / bf16 / int8)
+    or [ntiles, m, TW/2] uint8 (int4 nibbles, low = even column); int8 carries
+    a per-column scale [ntiles*TW], int4 a per (row group, column) scale
+    [ceil(m/group), ntiles*TW]."""
+
+    data: torch.Tensor
+    col_scale: torch.Tensor | None = None
+    gscale: torch.Tensor | None = None
+    group: int = 0
+
+    @property
+    def ntiles(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def dtype_code(self) -> int:
+        if self.data.dtype == torch.uint8:
+            return C.TEAL_I4
+        return RT.dtype_code(self.data.dtype)
+
+    def dequantize(self) -> torch.Tensor:
+        """fp32 [ntiles, m, TW] values the kernel multiplies with."""
+        d = self.data
+        nt, m = d.shape[0], d.shape[1]
+        if d.dtype == torch.int8:
+            return d.float() * self.col_scale.view(nt, 1, TW)
+        if d.dtype == torch.uint8:
+            lo = (d & 0xF).to(torch.int16)
+            hi = (d >> 4).to(torch.int16)
+            q = torch.stack([lo, hi], dim=-1).reshape(nt, m, TW)
+            q = torch.where(q >= 8, q - 16, q).float()
+            gi = torch.arange(m, device=d.device) // self.group
+            sc = self.gscale.view(-1, nt, TW)[gi]          # [m, nt, TW]
+            return q * sc.permute(1, 0, 2)
+        return d.float()
+
+
+def quantize_tiles(t: torch.Tensor, quant: str | None, group: int = 128) -> TiledW:
+    """Quantise tiled weights [ntiles, m, TW]: None keeps the dtype; 'int8'
+    symmetric per output column; 'int4' symmetric per (row group, column)."""
+    if quant is None:
+        return TiledW(t.contiguous())
+    w = t.float()
+    nt, m, tw = w.shape
+    if quant == "int8":
+        sc = w.abs().amax(dim=1) / 127.0                                   # [nt, TW]
+        sc = torch.where(sc > 0, sc, torch.ones_like(sc))
+        q = torch.clamp(torch.round(w / sc[:, None, :]), -127, 127).to(torch.int8)
+        return TiledW(q.contiguous(), col_scale=sc.reshape(-1).contiguous())
+    if quant == "int4":
+        ng = -(-m // group)
+        pad = ng * group - m
+        wp = torch.cat([w, torch.zeros(nt, pad, tw, device=w.device)], dim=1) if pad else w
+        sc = wp.view(nt, ng, group, tw).abs().amax(dim=2) / 7.0            # [nt, ng, TW]
+        sc = torch.where(sc > 0, sc, torch.ones_like(sc))
+        gi = torch.arange(m, device=w.device) // group
+        q = torch.clamp(torch.round(w / sc[:, gi, :]), -8, 7).to(torch.int16)
+        qu = (q & 0xF).to(torch.uint8).view(nt, m, tw // 2, 2)
+        packed = (qu[..., 0] | (qu[..., 1] << 4)).contiguous()
+        return TiledW(packed, gscale=sc.permute(1, 0, 2).reshape(ng, nt * tw).contiguous(), group=group)
+    raise ValueError(f"unknown quantisation {quant!r} (None, 'int8', 'int4')")
+
+
+def untile(t: torch.Tensor, n: int) -> torch.Tensor:
+    """[ntiles, m, TW] -> input-major [m, n]."""
+    nt, m, tw = t.shape
+    return t.permute(1, 0, 2).reshape(m, nt * tw)[:, :n].contiguous()
+
+
+def untile_gate_up(t: torch.Tensor, f: int) -> torch.Tensor:
+    """Interleaved gate|up tiles -> input-major [m, 2f] (gate columns, then up)."""
+    nt, m, tw = t.shape
+    g = t[:, :, : tw // 2].permute(1, 0, 2).reshape(m, -1)[:, :f]
+    u = t[:, :, tw // 2:].permute(1, 0, 2).reshape(m, -1)[:, :f]
+    return torch.cat([g, u], dim=1).contiguous()
+
+
 class StepDecoder:
     """TEAL decode for one sequence with one persistent launch per token.
 
@@ -143,7 +225,8 @@ class StepDecoder:
 
     def __init__(self, weights: DecoderWeights, thresholds=None, kv_dtype=None, device=None,
                  taps: bool = False, attn_chunk: int = 0, ctas: int = 0,
-                 count_kept: bool = False, attn_debug: bool = False):
+                 count_kept: bool = False, attn_debug: bool = False, prefetch_kb: int | None = None,
+                 quant: str | None = None):
         self.w = weights
         spec = self.spec = weights.spec
         dev = self.device = device or RT.require_cuda()
@@ -164,11 +247,15 @@ class StepDecoder:
         self.w_dtype = weights.dtype
         f32 = dict(device=dev, dtype=torch.float32)
         # tiled weights
+        self.quant = quant
         self.tw = []
         for lw in weights.layers:
-            self.tw.append(dict(qkv=pack_tiled(lw.wqkv), o=pack_tiled(lw.wo),
-                                gu=pack_gate_up(lw.wgu[:, :f], lw.wgu[:, f:]), down=pack_tiled(lw.wdown)))
-        self.lm_t = pack_tiled(weights.lm_head) if spec.vocab else None
+            self.tw.append(dict(qkv=quantize_tiles(pack_tiled(lw.wqkv), quant),
+                                o=quantize_tiles(pack_tiled(lw.wo), quant),
+                                gu=quantize_tiles(pack_gate_up(lw.wgu[:, :f], lw.wgu[:, f:]), quant),
+                                down=quantize_tiles(pack_tiled(lw.wdown), quant)))
+        self.lm_t = quantize_tiles(pack_tiled(weights.lm_head), quant) if spec.vocab else None
+        self.w_code = (self.tw[0]["qkv"].dtype_code if self.tw else RT.dtype_code(weights.dtype))
         # activations / state
         self.x = torch.zeros(d, **f32)
         self.x_in = torch.zeros(d, **f32)
@@ -200,6 +287,10 @@ class StepDecoder:
         # kept-channel counters accumulated over every step (for algorithmic bytes)
         self.kept = self.taps.kept if taps else (torch.zeros(L, 7, device=dev, dtype=torch.int64) if count_kept else None)
         self.ctas = ctas
+        if prefetch_kb is None:
+            import os
+            prefetch_kb = int(os.environ.get("TEAL_STEP_PREFETCH_KB", "0"))
+        self.prefetch_bytes = max(0, int(prefetch_kb)) * 1024
         self.attn_dbg = torch.zeros(spec.n_kv_heads * self.nchunks, 6, device=dev, dtype=torch.int64) if attn_debug else None
         self._build(thresholds)
         self.graph = None
@@ -215,7 +306,7 @@ class StepDecoder:
             raise ValueError(f"need {L} per-layer threshold lists of 7 (q,k,v,o,gate,up,down)")
         self.thresholds = thr
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        per = C.lib().teal_step_ctas_per_sm(RT.dtype_code(self.w_dtype))
+        per = C.lib().teal_step_ctas_per_sm(self.w_code)
         if per < 1:
             raise RuntimeError("teal step kernel cannot be resident on this device")
         self.grid = min(self.ctas, per * sms) if self.ctas > 0 else per * sms
@@ -313,7 +404,7 @@ class StepDecoder:
                                            [K[l, 6]] if K is not None else None)))
             phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_ROWS, cb["gu"], 1, TH))
         if spec.vocab:
-            nt_lm = self.lm_t.shape[0]
+            nt_lm = self.lm_t.ntiles
             mc_lm = max_contributors(nt_lm, d, Gc)
             self.ws["lm"] = torch.zeros(nt_lm * mc_lm * TW, device=dev)
             self.tk["lm"] = torch.zeros(max(4096, nt_lm), device=dev, dtype=torch.int32)
@@ -346,7 +437,8 @@ class StepDecoder:
         p.cand_v, p.cand_i, p.token_out, p.lm_done = (self.cand_v.data_ptr(), self.cand_i.data_ptr(),
                                                       self.token.data_ptr(), self.lm_done.data_ptr())
         p.nphases, p.ncounters, p.d = self.nphases, self.ncounters, d
-        p.w_dtype, p.ctas = RT.dtype_code(self.w_dtype), self.grid
+        p.w_dtype, p.ctas = self.w_code, self.grid
+        p.prefetch_bytes = self.prefetch_bytes
         self.plan = p
 
     def enable_timeline(self) -> torch.Tensor:
@@ -362,7 +454,8 @@ class StepDecoder:
                v_cache=None, y=None, dbg=None):
         spec = self.spec
         g = StepGroup()
-        g.w, g.tiles, g.x = wt.data_ptr(), tiles.data_ptr(), x.data_ptr()
+        g.w, g.tiles, g.x = wt.data.data_ptr(), tiles.data_ptr(), x.data_ptr()
+        g.col_scale, g.gscale, g.group = RT.ptr(wt.col_scale), RT.ptr(wt.gscale), wt.group
         g.gain = gain.data_ptr() if gain is not None else None
         g.ss = self.ss.data_ptr()
         g.partials, g.tickets = self.ws[ws].data_ptr(), self.tk[ws].data_ptr()
@@ -379,9 +472,10 @@ class StepDecoder:
                 g.dbg_bits[i] = b.data_ptr()
             for i, k in enumerate(kept or []):
                 g.kept[i] = k.data_ptr()
-        g.max_seq, g.m, g.n, g.ntiles, g.maxc = spec.max_seq, m, n, wt.shape[0], maxc
+        g.max_seq, g.m, g.n, g.ntiles, g.maxc = spec.max_seq, m, n, wt.ntiles, maxc
         g.prologue, g.nss, g.eps, g.epilogue = prologue, spec.d_model // TW, spec.norm_eps, epilogue
         g.nq, g.nkv, g.head_dim, g.kv_dtype = spec.n_q, spec.n_kv, spec.head_dim, RT.dtype_code(self.kv_dtype)
+        g.w_dtype = wt.dtype_code
         return g
 
     # -- step -----------------------------------------------------------------
@@ -402,7 +496,7 @@ class StepDecoder:
         LM head, + K and V reads of `positions` attended positions (summed
         over the steps)."""
         spec = self.spec
-        bw = self.tw[0]["qkv"].element_size()
+        bw = {C.TEAL_F32: 4, C.TEAL_BF16: 2, C.TEAL_I8: 1, C.TEAL_I4: 0.5}[self.w_code]
         shapes = spec.proj_shapes()
         kept = (self.kept if kept is None else kept).double().cpu()
         total = 0.0

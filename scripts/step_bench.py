@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=50)
 ap.add_argument("--ctas", type=int, default=0)
 ap.add_argument("--timeline", action="store_true")
+ap.add_argument("--quant", default="none")
 ap.add_argument("--layers", type=int, default=32)
 ap.add_argument("--engines", default="launch,step")
 a = ap.parse_args()
@@ -28,7 +29,7 @@ hists = D.calibrate_histograms(W, n_tokens=8)
 for s in (None, 0.5):
     thr = None if s is None else D.uniform_thresholds(hists, spec.n_layers, s)
     for eng in a.engines.split(","):
-        dec = (E.StepDecoder(W, thr, ctas=a.ctas, count_kept=True) if eng == "step"
+        dec = (E.StepDecoder(W, thr, ctas=a.ctas, count_kept=True, quant=None if a.quant == "none" else a.quant) if eng == "step"
                else D.SparseDecoder(W, thr))
         dec.reset()
         dec.capture()
@@ -49,7 +50,7 @@ for s in (None, 0.5):
         if eng == "step":
             byts = dec.algorithmic_bytes(dec.kept, steps=a.steps) / a.steps
             extra = f" algo {byts / 1e9:.3f} GB/step -> {byts / (ms * 1e-3) / 1e9:.0f} GB/s"
-        print(f"{eng:6s} s={s}: {ms:.3f} ms/token  {1e3 / ms:.1f} tok/s{extra}", flush=True)
+        print(f"{eng:6s} {a.quant:4s} s={s}: {ms:.3f} ms/token  {1e3 / ms:.1f} tok/s{extra}", flush=True)
         if eng == "step" and a.timeline:
             tl = dec.enable_timeline()
             dec.capture()

@@ -162,3 +162,38 @@ def test_llama_graph_replay_chains_tokens():
     # same weights, same thresholds: the greedy chains agree (fp32 accumulate
     # order differs between engines; logits are far from ties here)
     assert seq_a == seq_b
+
+
+@pytest.mark.parametrize("quant", ["int8", "int4"])
+@pytest.mark.parametrize("sparse", [False, True])
+def test_llama_style_quantised_weights(quant, sparse):
+    # int8 / int4 tiled rows (config 5 at batch 1): the step engine against a
+    # torch fp32 decode of the SAME dequantised weights (quantisation error
+    # itself is not part of the parity; SURVEY.md §8c "parity unpinned")
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200 import engine as E
+    from test_decode_gpu import torch_decode_reference
+    spec = D.DecoderSpec(1024, 8, 2, 2816, 2, vocab=1024, rope_theta=500000.0, norm_eps=1e-5, max_seq=64)
+    W = D.random_weights(spec, torch.bfloat16, seed=5)
+    thr = [[0.3, 0.4, 0.5, 0.02, 0.6, 0.7, 0.05]] * 2 if sparse else [[None] * 7] * 2
+    dec = E.StepDecoder(W, thr, kv_dtype=torch.float32, quant=quant, attn_chunk=16)
+    f, nq, nkv = spec.d_ff, spec.n_q, spec.n_kv
+    layers = []
+    for lw, tw in zip(W.layers, dec.tw):
+        layers.append(D.LayerWeights(
+            wqkv=E.untile(tw["qkv"].dequantize(), nq + 2 * nkv), wo=E.untile(tw["o"].dequantize(), spec.d_model),
+            wgu=E.untile_gate_up(tw["gu"].dequantize(), f), wdown=E.untile(tw["down"].dequantize(), spec.d_model),
+            rms_attn=lw.rms_attn, rms_mlp=lw.rms_mlp))
+    Wq = D.DecoderWeights(spec, layers, W.embedding, W.final_norm, E.untile(dec.lm_t.dequantize(), spec.vocab))
+    err_q = float((Wq.layers[0].wdown - W.layers[0].wdown.float()).norm() / W.layers[0].wdown.float().norm())
+    assert err_q < (0.02 if quant == "int8" else 0.2), err_q
+    dec.reset()
+    tokens = [5, 17, 999, 3, 250, 7, 7, 42, 11, 600]
+    ref = torch_decode_reference(Wq, thr, tokens, spec, torch.float32)
+    for i, tok in enumerate(tokens):
+        dec.token.fill_(tok)
+        dec.step_token()
+        torch.cuda.synchronize()
+        x_ref, logits_ref = ref[i]
+        assert rel_err(dec.x.cpu().numpy(), x_ref.cpu().numpy()) < 1e-3, (quant, i)
+        assert rel_err(dec.logits.cpu().numpy(), logits_ref.cpu().numpy()) < 1e-3, (quant, i)
