@@ -455,36 +455,47 @@ __device__ __forceinline__ void stream_rows(const unsigned char* tb, int cnt, co
     constexpr int ROWB = WFmt<WT>::ROWB;
     constexpr int LB = WFmt<WT>::LB;
     constexpr int HB = ROWB / 2;
-    // rows per pipeline stage: equal bytes in flight for every format (UB bf16 rows)
-    constexpr int U = WT == TEAL_F32 ? UB / 2 : (WT == TEAL_BF16 ? UB : (WT == TEAL_I8 ? 2 * UB : 4 * UB));
+    // rows per pipeline stage (int8 / int4 rows are narrower; measured: more
+    // rows per stage does not help them — their unpack is issue-bound)
+    constexpr int U = WT == TEAL_F32 ? UB / 2 : UB;
     constexpr int NW_ = LaneW<WT>::N;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int myhalf = lane < 16 ? 30 : 31;
+    // the lane's h values ride in registers with the loads (0 where this
+    // lane's half of the row is pruned)
+    constexpr int HN = U * (WT == TEAL_F32 ? 2 : 1);
     LaneW<WT> a[U], b[U];
+    float ha[HN], hb[HN];
     float accg[8];
     int curg = -1;
 #pragma unroll
     for (int j = 0; j < 8; ++j) accg[j] = 0.f;
     // loads only: the kept bits and h are re-read from shared memory when consumed
-    auto fetch = [&](int e0, LaneW<WT> (&d)[U]) {
+    auto fetch = [&](int e0, LaneW<WT> (&d)[U], float (&hh)[HN]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int e = e0 + u;
 #pragma unroll
             for (int k = 0; k < NW_; ++k) d[u].u[k] = 0u;
+            hh[u * (HN / U)] = 0.f;
+            if constexpr (WT == TEAL_F32) hh[2 * u + 1] = 0.f;
             if (e < cnt) {
                 const unsigned pk = (unsigned)s.u.g.idx[e];
                 const unsigned char* rp = tb + (int64_t)(pk & 0x3fffffffu) * ROWB;
                 if constexpr (WT == TEAL_F32) {
+                    const float hv = s.u.g.h[e];
                     if ((pk >> 30) & 1u) {
                         const uint4 r = ldw16(rp + lane * 16, pol);
                         d[u].u[0] = r.x; d[u].u[1] = r.y; d[u].u[2] = r.z; d[u].u[3] = r.w;
+                        hh[2 * u] = hv;
                     }
                     if ((pk >> 31) & 1u) {
                         const uint4 r = ldw16(rp + HB + lane * 16, pol);
                         d[u].u[4] = r.x; d[u].u[5] = r.y; d[u].u[6] = r.z; d[u].u[7] = r.w;
+                        hh[2 * u + 1] = hv;
                     }
                 } else if ((pk >> myhalf) & 1u) {
+                    hh[u] = s.u.g.h[e];
                     if constexpr (LB == 16) {
                         const uint4 r = ldw16(rp + lane * 16, pol);
                         d[u].u[0] = r.x; d[u].u[1] = r.y; d[u].u[2] = r.z; d[u].u[3] = r.w;
@@ -508,49 +519,44 @@ __device__ __forceinline__ void stream_rows(const unsigned char* tb, int cnt, co
             }
         }
     };
-    auto consume = [&](int e0, const LaneW<WT> (&d)[U]) {
+    auto consume = [&](int e0, const LaneW<WT> (&d)[U], const float (&hh)[HN]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int e = e0 + u;
-            if (e >= cnt) break;
-            const unsigned pk = (unsigned)s.u.g.idx[e];
-            const float hv = s.u.g.h[e];
             float w[8];
             unpack8<WT>(d[u], w);
             if constexpr (WT == TEAL_F32) {
-                const float h0 = ((pk >> 30) & 1u) ? hv : 0.f, h1 = ((pk >> 31) & 1u) ? hv : 0.f;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) acc[k] = fmaf(h0, w[k], acc[k]);
+                for (int k = 0; k < 4; ++k) acc[k] = fmaf(hh[2 * u], w[k], acc[k]);
 #pragma unroll
-                for (int k = 4; k < 8; ++k) acc[k] = fmaf(h1, w[k], acc[k]);
-            } else {
-                const float h = ((pk >> myhalf) & 1u) ? hv : 0.f;
-                if constexpr (WT == TEAL_I4) {
-                    const int gr = (gbase + (int)(pk & 0x3fffffffu)) / group;
+                for (int k = 4; k < 8; ++k) acc[k] = fmaf(hh[2 * u + 1], w[k], acc[k]);
+            } else if constexpr (WT == TEAL_I4) {
+                const int e = e0 + u;
+                if (e < cnt) {
+                    const int gr = (gbase + (int)((unsigned)s.u.g.idx[e] & 0x3fffffffu)) / group;
                     if (gr != curg) {
                         flush_group();
                         curg = gr;
                     }
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) accg[k] = fmaf(h, w[k], accg[k]);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) acc[k] = fmaf(h, w[k], acc[k]);
                 }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) accg[k] = fmaf(hh[u], w[k], accg[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc[k] = fmaf(hh[u], w[k], acc[k]);
             }
         }
     };
     int e0 = warp * U;
     if (e0 < cnt) {
-        fetch(e0, a);
+        fetch(e0, a, ha);
         for (;;) {
             const int en = e0 + NW * U;
-            if (en < cnt) fetch(en, b);
-            consume(e0, a);
+            if (en < cnt) fetch(en, b, hb);
+            consume(e0, a, ha);
             if (en >= cnt) break;
             e0 = en;
-            if (e0 + NW * U < cnt) fetch(e0 + NW * U, a);
-            consume(e0, b);
+            if (e0 + NW * U < cnt) fetch(e0 + NW * U, a, ha);
+            consume(e0, b, hb);
             if (e0 + NW * U >= cnt) break;
             e0 += NW * U;
         }
