@@ -53,6 +53,7 @@ constexpr int ATT_MAXG = 8;
 constexpr int ATT_MAXHD = 128;
 constexpr int ATT_MAXCHUNK = 256;
 constexpr int ATT_STAGE = 16384;  // bytes of K (and of V) staged per attention unit
+constexpr int ATT_MAXCHUNK_STAGE = 128;  // staged positions (>= 16384 / (hd * kv bytes))
 static_assert(NT == TW, "epilogues map one thread per tile column");
 
 struct Smem {
@@ -65,7 +66,7 @@ struct Smem {
         struct {
             float q[ATT_MAXG * ATT_MAXHD];
             float sc[ATT_MAXG * ATT_MAXCHUNK];
-            uint4 k[ATT_STAGE / 16];   // K rows of the chunk (raw cache dtype)
+            uint4 k[ATT_STAGE / 16 + 4 * ATT_MAXCHUNK_STAGE];  // K rows, each padded by 64 B (bank-conflict free)
             uint4 v[ATT_STAGE / 16];   // V rows of the chunk
         } a;
     } u;
@@ -371,7 +372,8 @@ __device__ __forceinline__ float rms_den(const teal_step_group& g, int lane) {
 __device__ __forceinline__ int participants(int ntiles, int64_t F) {
     const int grid = gridDim.x;
     if (F <= grid) return (int)F;
-    if (2 * ntiles <= grid) return ntiles * (grid / ntiles);
+    const int aligned = ntiles * (grid / ntiles);
+    if (2 * ntiles <= grid && 10 * aligned >= 9 * grid) return aligned;  // keep >= 90% of the grid busy
     return grid;
 }
 
@@ -674,7 +676,7 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
 template <typename KT>
 __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_step_attn& a, int g, int ch, Smem& s) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int G = a.H / a.KVH, hd = a.hd, ndc = (hd + 31) / 32;
+    const int G = a.H / a.KVH, hd = a.hd;
     const int L = __ldcg(P.state + 1);
     const int p0 = ch * a.chunk;
     const int p1 = min(L, p0 + a.chunk);
@@ -690,6 +692,7 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
         // 16-byte loads all in flight together: one L2/HBM round trip
         constexpr int KB = (int)sizeof(KT);
         const int n16 = np * hd * KB / 16;
+        const int vpr = hd * KB / 16;  // 16-byte vectors per K/V row
         const uint4* gk = reinterpret_cast<const uint4*>(reinterpret_cast<const KT*>(a.k_cache) + kvbase + (int64_t)p0 * hd);
         const uint4* gv = reinterpret_cast<const uint4*>(reinterpret_cast<const KT*>(a.v_cache) + kvbase + (int64_t)p0 * hd);
         for (int o = tid; o < G * hd; o += NT) s.u.a.q[o] = __ldcg(a.q + (int64_t)g * G * hd + o);
@@ -705,28 +708,70 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
 #pragma unroll
             for (int q = 0; q < PER; ++q) {
                 const int v = tid + q * NT;
-                if (v < n16) { s.u.a.k[v] = kk[q]; s.u.a.v[v] = vv[q]; }
+                if (v < n16) {
+                    s.u.a.k[(v / vpr) * (vpr + 4) + v % vpr] = kk[q];  // K row p at p*(vpr+4) (64-B pad)
+                    s.u.a.v[v] = vv[q];
+                }
             }
         }
         __syncthreads();
-        const KT* ks = reinterpret_cast<const KT*>(s.u.a.k);
+        ATT_STAMP(2);
         const KT* vs = reinterpret_cast<const KT*>(s.u.a.v);
         const float den = sqrtf((float)hd);
-        // scores: warp per position, lanes over head_dim
+        // scores: 4 threads per position; thread dq takes the row's 16-byte
+        // chunks dq, dq+4, ... (K rows padded by 64 B and the interleaved
+        // chunks make both the K and the q reads bank-conflict free); the K
+        // chunk is loaded once and used for every head; 2 shuffles combine.
+        {
+            const int dq = tid & 3, pl = tid >> 2;
+            constexpr int EPC = 16 / KB;  // elements per 16-byte chunk
 #pragma unroll 1
-        for (int p = warp; p < np; p += NW) {
-            float kr[ATT_MAXHD / 32];
+            for (int p = pl; p < (np + 63) / 64 * 64; p += NT / 4) {
+                const bool pv = p < np;
+                const uint4* kr = s.u.a.k + (pv ? p : 0) * (vpr + 4);
+                float dot[ATT_MAXG];
 #pragma unroll
-            for (int dc = 0; dc < ATT_MAXHD / 32; ++dc)
-                kr[dc] = (dc < ndc && lane + 32 * dc < hd) ? to_f32<KT>(ks[p * hd + lane + 32 * dc]) : 0.f;
+                for (int h = 0; h < ATT_MAXG; ++h) dot[h] = 0.f;
 #pragma unroll 1
-            for (int h = 0; h < G; ++h) {
-                float dot = 0.f;
+                for (int c = dq; c < vpr; c += 4) {
+                    const uint4 raw = kr[c];
+                    float kv[8];
+                    if constexpr (KB == 2) {
+                        const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
-                for (int dc = 0; dc < ATT_MAXHD / 32; ++dc)
-                    if (dc < ndc && lane + 32 * dc < hd) dot = fmaf(s.u.a.q[h * hd + lane + 32 * dc], kr[dc], dot);
-                dot = warp_sum(dot);
-                if (lane == 0) s.u.a.sc[h * ATT_MAXCHUNK + p] = dot / den;
+                        for (int k = 0; k < 4; ++k) { kv[2 * k] = bf16_lo(u[k]); kv[2 * k + 1] = bf16_hi(u[k]); }
+                    } else {
+                        kv[0] = __uint_as_float(raw.x); kv[1] = __uint_as_float(raw.y);
+                        kv[2] = __uint_as_float(raw.z); kv[3] = __uint_as_float(raw.w);
+                    }
+#pragma unroll
+                    for (int h = 0; h < ATT_MAXG; ++h) {
+                        if (h < G) {
+                            const float4* qv = reinterpret_cast<const float4*>(s.u.a.q + h * hd + c * EPC);
+                            const float4 q0 = qv[0];
+                            dot[h] = fmaf(q0.x, kv[0], dot[h]);
+                            dot[h] = fmaf(q0.y, kv[1], dot[h]);
+                            dot[h] = fmaf(q0.z, kv[2], dot[h]);
+                            dot[h] = fmaf(q0.w, kv[3], dot[h]);
+                            if constexpr (EPC == 8) {
+                                const float4 q1 = qv[1];
+                                dot[h] = fmaf(q1.x, kv[4], dot[h]);
+                                dot[h] = fmaf(q1.y, kv[5], dot[h]);
+                                dot[h] = fmaf(q1.z, kv[6], dot[h]);
+                                dot[h] = fmaf(q1.w, kv[7], dot[h]);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < ATT_MAXG; ++h) {
+                    if (h < G) {
+                        float d = dot[h];
+                        d += __shfl_xor_sync(0xffffffffu, d, 1);
+                        d += __shfl_xor_sync(0xffffffffu, d, 2);
+                        if (pv && dq == 0) s.u.a.sc[h * ATT_MAXCHUNK + p] = d / den;
+                    }
+                }
             }
         }
         __syncthreads();
@@ -751,17 +796,35 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
         // single chunk holding every position is final: normalise and write
         // the context directly (no partial record, ticket or combine).
         const bool single = (p0 == 0 && p1 == L);
-#pragma unroll 1
-        for (int o = tid; o < G * hd; o += NT) {
-            const int h = o / hd, d = o - h * hd;
-            const float* pr = s.u.a.sc + h * ATT_MAXCHUNK;
-            float acc = 0.f;
+        {  // thread -> column d and heads hs, hs + NT/hd, ...: each V element read once for its heads
+            const int hstep = NT / hd > 0 ? NT / hd : 1;
+            const int d = tid % hd, hs = tid / hd;
+            if (hs < hstep) {
+                float acc[ATT_MAXG];
+#pragma unroll
+                for (int k = 0; k < ATT_MAXG; ++k) acc[k] = 0.f;
 #pragma unroll 4
-            for (int p = 0; p < np; ++p) acc = fmaf(pr[p], to_f32<KT>(vs[p * hd + d]), acc);
-            if (single) a.ctx[(int64_t)g * G * hd + o] = acc / s.al[h];
-            else __stcg(my + o, acc);
+                for (int p = 0; p < np; ++p) {
+                    const float vv = to_f32<KT>(vs[p * hd + d]);
+#pragma unroll
+                    for (int k = 0; k < ATT_MAXG; ++k) {
+                        const int h = hs + k * hstep;
+                        if (h < G) acc[k] = fmaf(s.u.a.sc[h * ATT_MAXCHUNK + p], vv, acc[k]);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < ATT_MAXG; ++k) {
+                    const int h = hs + k * hstep;
+                    if (h < G) {
+                        const int o = h * hd + d;
+                        if (single) a.ctx[(int64_t)g * G * hd + o] = acc[k] / s.al[h];
+                        else __stcg(my + o, acc[k]);
+                    }
+                }
+            }
         }
         if (single) {
+            ATT_STAMP(3);
             ATT_STAMP(4);
             signal(P.counters, a.sig_base + g, a.sig_base + g);
             ATT_STAMP(5);

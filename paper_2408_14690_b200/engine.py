@@ -78,8 +78,9 @@ def participants(ntiles: int, F: int, grid: int) -> int:
     """CTAs taking part in a GEMV phase (csrc/teal_step.cu participants())."""
     if F <= grid:
         return F
-    if 2 * ntiles <= grid:
-        return ntiles * (grid // ntiles)
+    aligned = ntiles * (grid // ntiles)
+    if 2 * ntiles <= grid and 10 * aligned >= 9 * grid:
+        return aligned
     return grid
 
 
