@@ -796,32 +796,20 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
         // single chunk holding every position is final: normalise and write
         // the context directly (no partial record, ticket or combine).
         const bool single = (p0 == 0 && p1 == L);
-        {  // thread -> column d and heads hs, hs + NT/hd, ...: each V element read once for its heads
-            const int hstep = NT / hd > 0 ? NT / hd : 1;
-            const int d = tid % hd, hs = tid / hd;
-            if (hs < hstep) {
-                float acc[ATT_MAXG];
-#pragma unroll
-                for (int k = 0; k < ATT_MAXG; ++k) acc[k] = 0.f;
+#pragma unroll 1
+        for (int o = tid; o < G * hd; o += NT) {
+            const int h = o / hd, d = o - h * hd;
+            const float* pr = s.u.a.sc + h * ATT_MAXCHUNK;
+            float acc0 = 0.f, acc1 = 0.f;  // two chains (even / odd positions), summed at the end
 #pragma unroll 4
-                for (int p = 0; p < np; ++p) {
-                    const float vv = to_f32<KT>(vs[p * hd + d]);
-#pragma unroll
-                    for (int k = 0; k < ATT_MAXG; ++k) {
-                        const int h = hs + k * hstep;
-                        if (h < G) acc[k] = fmaf(s.u.a.sc[h * ATT_MAXCHUNK + p], vv, acc[k]);
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < ATT_MAXG; ++k) {
-                    const int h = hs + k * hstep;
-                    if (h < G) {
-                        const int o = h * hd + d;
-                        if (single) a.ctx[(int64_t)g * G * hd + o] = acc[k] / s.al[h];
-                        else __stcg(my + o, acc[k]);
-                    }
-                }
+            for (int p = 0; p + 1 < np; p += 2) {
+                acc0 = fmaf(pr[p], to_f32<KT>(vs[p * hd + d]), acc0);
+                acc1 = fmaf(pr[p + 1], to_f32<KT>(vs[(p + 1) * hd + d]), acc1);
             }
+            if (np & 1) acc0 = fmaf(pr[np - 1], to_f32<KT>(vs[(np - 1) * hd + d]), acc0);
+            const float acc = acc0 + acc1;
+            if (single) a.ctx[(int64_t)g * G * hd + o] = acc / s.al[h];
+            else __stcg(my + o, acc);
         }
         if (single) {
             ATT_STAMP(3);
