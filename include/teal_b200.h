@@ -298,7 +298,9 @@ typedef struct teal_step_group {
     int w_dtype;             /* TEAL_F32 / TEAL_BF16 / TEAL_I8 (col_scale) / TEAL_I4 (gscale) */
     const float* gscale;     /* TEAL_I4: [ceil(m/group)][ntiles*TW] fp32      */
     int group;               /* TEAL_I4 row-group size (>= 128)              */
-    int pad2_;
+    float t_all;             /* tiles == NULL: one threshold for every tile  */
+    int64_t tile_stride_b;   /* row_stride_b == 0: tiled (m*TW*esz, TW*esz)   */
+    int64_t row_stride_b;    /* else untiled input-major: TW*esz, ldw*esz    */
 } teal_step_group;
 
 typedef struct teal_step_attn {

@@ -34,6 +34,9 @@
 
 namespace teal {
 
+int step_gemv_eligible(const teal_gemv_args* a, int64_t* ws_floats, int64_t* tickets, int* grid_out);
+int step_gemv_single(const teal_gemv_args* a, cudaStream_t stream);
+
 constexpr int NT_MAX = 4;  // max column tiles one CTA's range may span
 
 struct KParams {
@@ -884,9 +887,16 @@ int teal_gemv_workspace(const teal_gemv_args* a, int* ctas, int64_t* ws_floats, 
     KParams P;
     memset(&P, 0, sizeof(P));
     plan(a, &P);
+    int64_t wsf = (int64_t)P.ntiles * P.maxc * P.tile, ntk = P.ntiles;
+    int64_t wsf2 = 0, ntk2 = 0;
+    int g2 = 0;
+    if (teal::step_gemv_eligible(a, &wsf2, &ntk2, &g2) == 0) {  // single-GEMV path sizes
+        if (wsf2 > wsf) wsf = wsf2;
+        if (ntk2 > ntk) ntk = ntk2;
+    }
     if (ctas) *ctas = P.G;
-    if (ws_floats) *ws_floats = (int64_t)P.ntiles * P.maxc * P.tile;
-    if (tickets) *tickets = P.ntiles;
+    if (ws_floats) *ws_floats = wsf;
+    if (tickets) *tickets = ntk;
     return TEAL_OK;
 }
 
@@ -924,6 +934,9 @@ int teal_fused_gemv(const teal_gemv_args* a, cudaStream_t stream) {
         TEAL_REQUIRE(P.tile % a->head_dim == 0 && a->seg[0].n % a->head_dim == 0 && a->seg[1].n % a->head_dim == 0,
                      "teal_fused_gemv: QKV epilogue needs head_dim | tile (%d) and head_dim | n", P.tile);
     TEAL_REQUIRE(a->ws && a->tickets, "teal_fused_gemv: ws and tickets are required");
+    // plain single-projection calls run on the persistent step kernel's streaming core
+    if (getenv("TEAL_OLD_GEMV") == nullptr && teal::step_gemv_eligible(a, nullptr, nullptr, nullptr) == 0)
+        return teal::step_gemv_single(a, stream);
     const bool xb = (a->x_dtype == TEAL_BF16);
     if (a->w_dtype == TEAL_BF16) return xb ? launch<uint16_t, uint16_t>(P, stream) : launch<uint16_t, float>(P, stream);
     if (a->w_dtype == TEAL_F32) return xb ? launch<float, uint16_t>(P, stream) : launch<float, float>(P, stream);

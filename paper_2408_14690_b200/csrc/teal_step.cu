@@ -174,11 +174,23 @@ __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Tile thresholds / signals: the plan's per-tile table, or (tiles == NULL,
+// single-GEMV launches) one threshold for every tile and no signals.
+__device__ __forceinline__ teal_step_tile tile_meta(const teal_step_group& g, int tile) {
+    if (g.tiles) return g.tiles[tile];
+    teal_step_tile t;
+    t.t_lo = t.t_hi = g.t_all;
+    t.seg_lo = t.seg_hi = 0;
+    t.first_lo = t.first_hi = tile == 0;
+    t.sig0 = t.sig1 = -1;
+    return t;
+}
+
 // ---- epilogue of one finished column tile (thread c = column c) --------------
 __device__ __noinline__ void finalize(const teal_step_plan& P, const teal_step_group& g, int tile, float v, Smem& s) {
     const int c = threadIdx.x;
     const int64_t col = (int64_t)tile * TW + c;
-    const teal_step_tile tm = g.tiles[tile];
+    const teal_step_tile tm = tile_meta(g, tile);
     switch (g.epilogue) {
         case TEAL_SEPI_STORE: {
             if (col < g.n) g.y[col] = v;
@@ -452,8 +464,8 @@ __device__ int compact_rows(const teal_step_group& g, const teal_step_tile& tm, 
 // every lane loads 16 B of each kept half).  int4 rows accumulate per row
 // group and are scaled when the group changes (scales staged in s.u.g.gsc).
 template <int WT, int UB>
-__device__ __forceinline__ void stream_rows(const unsigned char* tb, int cnt, const Smem& s, float acc[8],
-                                            uint64_t pol, int gbase, int group) {
+__device__ __forceinline__ void stream_rows(const unsigned char* tb, int64_t rsb, int cnt, const Smem& s, float acc[8],
+                                            uint64_t pol, int gbase, int group, bool ok_lo, bool ok_hi) {
     constexpr int ROWB = WFmt<WT>::ROWB;
     constexpr int LB = WFmt<WT>::LB;
     constexpr int HB = ROWB / 2;
@@ -483,20 +495,20 @@ __device__ __forceinline__ void stream_rows(const unsigned char* tb, int cnt, co
             if constexpr (WT == TEAL_F32) hh[2 * u + 1] = 0.f;
             if (e < cnt) {
                 const unsigned pk = (unsigned)s.u.g.idx[e];
-                const unsigned char* rp = tb + (int64_t)(pk & 0x3fffffffu) * ROWB;
+                const unsigned char* rp = tb + (int64_t)(pk & 0x3fffffffu) * rsb;
                 if constexpr (WT == TEAL_F32) {
                     const float hv = s.u.g.h[e];
-                    if ((pk >> 30) & 1u) {
+                    if (((pk >> 30) & 1u) && ok_lo) {
                         const uint4 r = ldw16(rp + lane * 16, pol);
                         d[u].u[0] = r.x; d[u].u[1] = r.y; d[u].u[2] = r.z; d[u].u[3] = r.w;
                         hh[2 * u] = hv;
                     }
-                    if ((pk >> 31) & 1u) {
+                    if (((pk >> 31) & 1u) && ok_hi) {
                         const uint4 r = ldw16(rp + HB + lane * 16, pol);
                         d[u].u[4] = r.x; d[u].u[5] = r.y; d[u].u[6] = r.z; d[u].u[7] = r.w;
                         hh[2 * u + 1] = hv;
                     }
-                } else if ((pk >> myhalf) & 1u) {
+                } else if (((pk >> myhalf) & 1u) && ok_lo) {
                     hh[u] = s.u.g.h[e];
                     if constexpr (LB == 16) {
                         const uint4 r = ldw16(rp + lane * 16, pol);
@@ -610,8 +622,17 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
         if (ph.dep_kind == TEAL_DEP_ROWS)
             wait_range(P.counters, ph.dep + r0 / ph.dep_rows, ph.dep + (r1 - 1) / ph.dep_rows, ph.target);
         if (segi == 0) SL_STAMP(2, gtimer());
-        const teal_step_tile tm = g.tiles[tile];
-        const unsigned char* tbase = reinterpret_cast<const unsigned char*>(g.w) + (int64_t)tile * g.m * ROWB;
+        const teal_step_tile tm = tile_meta(g, tile);
+        // tiled: tile t = block [m][TW]; untiled input-major (single GEMV): row stride ldw
+        const int64_t rsb = g.row_stride_b ? g.row_stride_b : ROWB;
+        const int64_t tsb = g.row_stride_b ? g.tile_stride_b : (int64_t)g.m * ROWB;
+        const unsigned char* tbase = reinterpret_cast<const unsigned char*>(g.w) + (int64_t)tile * tsb;
+        // untiled matrices: lanes whose columns lie past n (last tile) load
+        // nothing; tiled blocks are zero-padded to whole tiles
+        const int64_t c0 = (int64_t)tile * TW;
+        const bool untiled = g.row_stride_b != 0;
+        const bool ok_lo = !untiled || ((WT == TEAL_F32) ? (c0 + 4 * lane < g.n) : (c0 + 8 * lane < g.n));
+        const bool ok_hi = !untiled || ((WT == TEAL_F32) ? (c0 + TH + 4 * lane < g.n) : ok_lo);
         float acc[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] = 0.f;
@@ -624,7 +645,8 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
                     s.u.g.gsc[q] = __ldg(g.gscale + (int64_t)(gA + q / TW) * g.ntiles * TW + (int64_t)tile * TW + q % TW);
                 __syncthreads();
             }
-            stream_rows<WT, UB>(tbase + (int64_t)ra * ROWB, cnt, s, acc, pol, ra, g.group > 0 ? g.group : 1);
+            stream_rows<WT, UB>(tbase + (int64_t)ra * rsb, rsb, cnt, s, acc, pol, ra, g.group > 0 ? g.group : 1,
+                                ok_lo, ok_hi);
             __syncthreads();  // rows list is rewritten by the next chunk
         }
         SL_STAMP(segi == 0 ? 3 : 5, gtimer());
@@ -1011,7 +1033,126 @@ static int occupancy(int w_dtype) {
     return cache;
 }
 
+// ---- single sparse/dense GEMV on the step streaming core -----------------------
+// y = s_t(x) W^T over an UNTILED input-major W (row stride ldw): one ordinary
+// launch with a single GEMV phase (no dependencies, no signals), split tiles
+// combined by tickets.  Used by teal_fused_gemv for plain single-projection
+// calls (kernel.sparse_gemv, matmul_dense, the GEMV sweep).
+struct OneArgs {
+    teal_step_plan P;
+    teal_step_group g;
+    teal_step_phase ph;
+};
+
+template <int WT, int MINB, int UB>
+__global__ void __launch_bounds__(NT, MINB) gemv_one_kernel(const __grid_constant__ OneArgs A) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+    const uint64_t pol = l2_evict_first_policy();
+    gemv_slice_t<WT, UB>(A.P, A.ph, A.g, s, pol, nullptr);
+}
+
+template <int WT>
+static void* one_kernel_ptr() { return (void*)gemv_one_kernel<WT, 2, 8>; }
+
+static int max_contrib(int ntiles, int m, int G) {
+    const int64_t gpt = (m + 31) / 32, F = (int64_t)ntiles * gpt;
+    int mc = 1;
+    for (int t = 0; t < ntiles; ++t) {
+        const int cf = (int)(((int64_t)t * gpt + 1) * G - 1) / F;
+        const int cl = (int)((((int64_t)t + 1) * gpt) * G - 1) / F;
+        if (cl - cf + 1 > mc) mc = cl - cf + 1;
+    }
+    return mc;
+}
+
+// participants() on the host (mirror of the device rule)
+static int host_participants(int ntiles, int64_t F, int grid) {
+    if (F <= grid) return (int)F;
+    const int aligned = ntiles * (grid / ntiles);
+    if (2 * ntiles <= grid && 10 * aligned >= 9 * grid) return aligned;
+    return grid;
+}
+
 }  // namespace step
+
+// eligibility + workspace of the single-GEMV path (-1: not eligible)
+int step_gemv_eligible(const teal_gemv_args* a, int64_t* ws_floats, int64_t* tickets, int* grid_out) {
+    using namespace step;
+    if (!a || a->nseg != 1 || a->prologue != TEAL_PRO_PLAIN || a->epilogue != TEAL_EPI_STORE) return -1;
+    if (a->x_dtype != TEAL_F32) return -1;
+    if (a->w_dtype != TEAL_BF16 && a->w_dtype != TEAL_F32 && a->w_dtype != TEAL_I8) return -1;
+    const teal_seg& sg = a->seg[0];
+    if (sg.n % 8 || sg.ldw % 8 || (reinterpret_cast<uintptr_t>(sg.w) & 15) || sg.dbg_bits) return -1;
+    if (a->m > (1 << 29)) return -1;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+    cudaGetLastError();
+    int grid = a->ctas > 0 ? a->ctas : 2 * sms;
+    const int ntiles = (int)((sg.n + TW - 1) / TW);
+    const int64_t F = (int64_t)ntiles * ((a->m + 31) / 32);
+    grid = (int)min64(grid, F);
+    const int G = host_participants(ntiles, F, grid);
+    if (ws_floats) *ws_floats = (int64_t)ntiles * max_contrib(ntiles, (int)a->m, G) * TW;
+    if (tickets) *tickets = ntiles;
+    if (grid_out) *grid_out = grid;
+    return 0;
+}
+
+int step_gemv_single(const teal_gemv_args* a, cudaStream_t stream) {
+    using namespace step;
+    int grid = 0;
+    int64_t wsf = 0, ntk = 0;
+    if (step_gemv_eligible(a, &wsf, &ntk, &grid) != 0) return -1;
+    const teal_seg& sg = a->seg[0];
+    OneArgs A;
+    memset(&A, 0, sizeof(A));
+    teal_step_group& g = A.g;
+    const int esz = a->w_dtype == TEAL_F32 ? 4 : (a->w_dtype == TEAL_BF16 ? 2 : 1);
+    g.w = sg.w;
+    g.col_scale = sg.col_scale;
+    g.tiles = nullptr;
+    g.t_all = sg.t32;
+    g.x = reinterpret_cast<const float*>(a->x);
+    g.partials = a->ws;
+    g.tickets = a->tickets;
+    g.y = sg.y;
+    g.kept[0] = sg.kept;
+    g.m = (int)a->m;
+    g.n = (int)sg.n;
+    g.ntiles = (int)((sg.n + TW - 1) / TW);
+    const int64_t F = (int64_t)g.ntiles * ((a->m + 31) / 32);
+    g.maxc = max_contrib(g.ntiles, g.m, host_participants(g.ntiles, F, grid));
+    g.prologue = TEAL_PRO_PLAIN;
+    g.epilogue = TEAL_SEPI_STORE;
+    g.w_dtype = a->w_dtype;
+    g.row_stride_b = sg.ldw * esz;
+    g.tile_stride_b = (int64_t)TW * esz;
+    A.ph.kind = TEAL_PHASE_GEMV;
+    A.ph.dep_kind = TEAL_DEP_NONE;
+    A.ph.dep_rows = 1;
+    void* k = a->w_dtype == TEAL_BF16 ? one_kernel_ptr<TEAL_BF16>()
+              : a->w_dtype == TEAL_F32 ? one_kernel_ptr<TEAL_F32>() : one_kernel_ptr<TEAL_I8>();
+    static bool attr_done[4] = {false, false, false, false};
+    if (!attr_done[a->w_dtype & 3]) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        attr_done[a->w_dtype & 3] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* args[1] = {(void*)&A};
+    cudaLaunchKernelExC(&cfg, k, args);
+    return check_launch("teal_sparse_gemv");
+}
+
 }  // namespace teal
 
 using namespace teal;

@@ -48,7 +48,7 @@ class StepGroup(ctypes.Structure):
                 ("max_seq", c_i64), ("m", c_i), ("n", c_i), ("ntiles", c_i), ("maxc", c_i),
                 ("prologue", c_i), ("nss", c_i), ("eps", c_f), ("epilogue", c_i),
                 ("nq", c_i), ("nkv", c_i), ("head_dim", c_i), ("kv_dtype", c_i), ("w_dtype", c_i),
-                ("gscale", c_vp), ("group", c_i), ("pad2_", c_i)]
+                ("gscale", c_vp), ("group", c_i), ("t_all", c_f), ("tile_stride_b", c_i64), ("row_stride_b", c_i64)]
 
 
 class StepAttn(ctypes.Structure):
