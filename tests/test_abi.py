@@ -71,7 +71,8 @@ def test_gemv_workspace_plan():
         tile = 512 if (dt == torch.bfloat16 and n % 16 == 0) else 256
         tiles = -(-n // tile)
         groups = tiles * (-(-m // 32))
-        assert 1 <= g <= groups and ntk == tiles and nws >= tiles * tile
+        # the workspace covers both the fused kernel and the single-GEMV step path
+        assert 1 <= g <= groups and ntk >= tiles and nws >= tiles * tile
 
 
 def test_traffic_model_matches_reference():
