@@ -412,21 +412,26 @@ PROJ_TAP = {"q": "pre_attn", "k": "pre_attn", "v": "pre_attn", "o": "attn_out",
             "gate": "pre_mlp", "up": "pre_mlp", "down": "mlp_inter"}
 
 
-def calibrate_histograms(weights: DecoderWeights, n_tokens: int = 16, seed: int = 0,
-                         bins: int | None = None, hi_std_multiple: float | None = None):
+def calibrate_histograms(weights, n_tokens: int = 16, seed: int = 0,
+                         bins: int | None = None, hi_std_multiple: float | None = None, engine: str = "launch"):
     """GPU-side calibration of the decode engine (model.py:268-294 restated for
     the KV-cache decode): run ``n_tokens`` dense decode steps on random tokens
     with the four taps captured, and bin each (layer, tap) vector on the GPU
     (``teal_hist_record``).  ``hi`` = HI_STD_MULTIPLE * std of the first
     step's tap, as the reference takes it from the first calibration sequence
-    (model.py:286-291).  Returns {(layer, tap): ActivationHistogram}."""
+    (model.py:286-291).  ``engine='step'`` runs the persistent engine (and
+    accepts pre-tiled weights).  Returns {(layer, tap): ActivationHistogram}."""
     from .sparsifier import DEFAULT_BIN_COUNT, HI_STD_MULTIPLE, ActivationHistogram
     bins = bins or DEFAULT_BIN_COUNT
     mult = hi_std_multiple or HI_STD_MULTIPLE
     spec = weights.spec
     if not spec.vocab:
         raise ValueError("token calibration needs an embedding (vocab > 0)")
-    dec = SparseDecoder(weights, None, taps=True)
+    if engine == "step":
+        from .engine import StepDecoder
+        dec = StepDecoder(weights, None, taps=True)
+    else:
+        dec = SparseDecoder(weights, None, taps=True)
     dec.reset()
     g = torch.Generator(device=dec.device).manual_seed(seed)
     toks = torch.randint(0, spec.vocab, (n_tokens,), device=dec.device, generator=g, dtype=torch.int32)

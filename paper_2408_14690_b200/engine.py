@@ -217,6 +217,69 @@ def untile_gate_up(t: torch.Tensor, f: int) -> torch.Tensor:
     return torch.cat([g, u], dim=1).contiguous()
 
 
+@dataclass
+class TiledModel:
+    """Decoder weights generated directly in the tiled layout (no untiled
+    copy: Llama-3-70B bf16 fits one B200 only this way).  `layers[l]` holds
+    the norm gains (rms_attn, rms_mlp), `tiles[l]` the TiledW groups."""
+
+    spec: object
+    layers: list
+    tiles: list
+    embedding: torch.Tensor | None
+    final_norm: torch.Tensor | None
+    lm: TiledW | None
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.embedding.dtype if self.embedding is not None else torch.bfloat16
+
+
+def random_tiled_model(spec, dtype=torch.bfloat16, seed: int = 0, device=None, quant: str | None = None,
+                       pool_gb: float = 2.0) -> TiledModel:
+    """Random-init tiled weights W ~ N(0, 1/d_in) (model.py:116-117 scale).
+    Values are copied out of one seeded pool of Gaussian samples at rotating
+    offsets (HBM copy speed instead of RNG speed for 140 GB), which keeps
+    every tile's rows distinct."""
+    from types import SimpleNamespace
+    dev = device or RT.require_cuda()
+    g = torch.Generator(device=dev).manual_seed(seed)
+    pool = torch.randn(int(pool_gb * (1 << 30)) // 2, device=dev, generator=g, dtype=torch.float32).to(dtype)
+    state = {"off": 0}
+    prime = 1000003
+
+    def fill(nt, m, tw, scale):
+        t = torch.empty(nt, m, tw, device=dev, dtype=dtype)
+        flat = t.view(-1)
+        pos = 0
+        while pos < flat.numel():
+            n = min(flat.numel() - pos, pool.numel() // 2)
+            o = state["off"] % (pool.numel() - n)
+            flat[pos:pos + n] = pool[o:o + n]
+            state["off"] += prime * 7919 + n // 3
+            pos += n
+        t.mul_(scale)
+        return quantize_tiles(t, quant)
+
+    d, f = spec.d_model, spec.d_ff
+    nq, nkv = spec.n_q, spec.n_kv
+    layers, tiles = [], []
+    for _ in range(spec.n_layers):
+        layers.append(SimpleNamespace(rms_attn=torch.ones(d, device=dev), rms_mlp=torch.ones(d, device=dev)))
+        tiles.append(dict(qkv=fill(-(-(nq + 2 * nkv) // TW), d, TW, d ** -0.5), o=fill(d // TW, nq, TW, nq ** -0.5),
+                          gu=fill(f // TH, d, TW, d ** -0.5), down=fill(d // TW, f, TW, f ** -0.5)))
+    emb = fin = lm = None
+    if spec.vocab:
+        emb = torch.empty(spec.vocab, d, device=dev, dtype=dtype)
+        for r in range(0, spec.vocab, 8192):
+            emb[r:r + 8192] = torch.randn(min(8192, spec.vocab - r), d, device=dev, generator=g).to(dtype)
+        fin = torch.ones(d, device=dev)
+        lm = fill(-(-spec.vocab // TW), d, TW, d ** -0.5)
+    del pool
+    torch.cuda.empty_cache()
+    return TiledModel(spec, layers, tiles, emb, fin, lm)
+
+
 class StepDecoder:
     """TEAL decode for one sequence with one persistent launch per token.
 
@@ -224,7 +287,7 @@ class StepDecoder:
     (thresholds per layer in the order q,k,v,o,gate,up,down; None or -inf =
     dense for that projection)."""
 
-    def __init__(self, weights: DecoderWeights, thresholds=None, kv_dtype=None, device=None,
+    def __init__(self, weights, thresholds=None, kv_dtype=None, device=None,
                  taps: bool = False, attn_chunk: int = 0, ctas: int = 0,
                  count_kept: bool = False, attn_debug: bool = False, prefetch_kb: int | None = None,
                  quant: str | None = None):
@@ -249,13 +312,17 @@ class StepDecoder:
         f32 = dict(device=dev, dtype=torch.float32)
         # tiled weights
         self.quant = quant
-        self.tw = []
-        for lw in weights.layers:
-            self.tw.append(dict(qkv=quantize_tiles(pack_tiled(lw.wqkv), quant),
-                                o=quantize_tiles(pack_tiled(lw.wo), quant),
-                                gu=quantize_tiles(pack_gate_up(lw.wgu[:, :f], lw.wgu[:, f:]), quant),
-                                down=quantize_tiles(pack_tiled(lw.wdown), quant)))
-        self.lm_t = quantize_tiles(pack_tiled(weights.lm_head), quant) if spec.vocab else None
+        if isinstance(weights, TiledModel):  # already tiled (and quantised): use as is
+            self.tw = weights.tiles
+            self.lm_t = weights.lm
+        else:
+            self.tw = []
+            for lw in weights.layers:
+                self.tw.append(dict(qkv=quantize_tiles(pack_tiled(lw.wqkv), quant),
+                                    o=quantize_tiles(pack_tiled(lw.wo), quant),
+                                    gu=quantize_tiles(pack_gate_up(lw.wgu[:, :f], lw.wgu[:, f:]), quant),
+                                    down=quantize_tiles(pack_tiled(lw.wdown), quant)))
+            self.lm_t = quantize_tiles(pack_tiled(weights.lm_head), quant) if spec.vocab else None
         self.w_code = (self.tw[0]["qkv"].dtype_code if self.tw else RT.dtype_code(weights.dtype))
         # activations / state
         self.x = torch.zeros(d, **f32)
