@@ -108,27 +108,35 @@ __device__ __forceinline__ void wait_range(const int* counters, int c0, int c1, 
 // orders every thread's writes before thread 0, whose gpu-scope fence makes
 // them (cumulatively) visible before its atomics — the cooperative-groups
 // grid-sync pattern, one fence per CTA instead of one per thread.
+// The barrier orders the CTA's writes before thread 0 (CTA scope); thread
+// 0's gpu-scope RELEASE reduction is cumulative over them, so no separate
+// sequentially-consistent fence (and L1 invalidation) is needed.
+__device__ __forceinline__ void red_release(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_acq_rel_add(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ void signal(int* counters, int c0, int c1) {
     __syncthreads();
-    if (threadIdx.x == 0 && c0 >= 0) {
-        __threadfence();
-        for (int c = c0; c <= c1; ++c) atomicAdd(counters + (int64_t)c * CSTRIDE, 1);
-    }
+    if (threadIdx.x == 0 && c0 >= 0)
+        for (int c = c0; c <= c1; ++c) red_release(counters + (int64_t)c * CSTRIDE, 1);
 }
 
 // Take a split-K ticket after storing this CTA's partial: returns (to every
 // thread) whether this CTA arrived last; the last arriver's thread 0 fences
 // again (acquire side) before the barrier that precedes the partial reads.
+// (acq_rel: releases this CTA's partial, and the last arriver acquires every
+// other contributor's before the barrier that precedes its partial reads)
 __device__ __forceinline__ bool take_ticket(unsigned* ticket, unsigned expected_prev, int& s_last) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned prev = atomicAdd(ticket, 1u);
+        const unsigned prev = atom_acq_rel_add(ticket, 1u);
         const int last = prev == expected_prev;
-        if (last) {
-            *ticket = 0u;
-            __threadfence();
-        }
+        if (last) *ticket = 0u;
         s_last = last;
     }
     __syncthreads();
@@ -187,7 +195,10 @@ __device__ __forceinline__ teal_step_tile tile_meta(const teal_step_group& g, in
 }
 
 // ---- epilogue of one finished column tile (thread c = column c) --------------
-__device__ __noinline__ void finalize(const teal_step_plan& P, const teal_step_group& g, int tile, float v, Smem& s) {
+// `pre`: the residual value of this column, loaded by the caller together
+// with the split-K partials (RESID epilogue).
+__device__ __noinline__ void finalize(const teal_step_plan& P, const teal_step_group& g, int tile, float v, Smem& s,
+                                      float pre) {
     const int c = threadIdx.x;
     const int64_t col = (int64_t)tile * TW + c;
     const teal_step_tile tm = tile_meta(g, tile);
@@ -199,7 +210,7 @@ __device__ __noinline__ void finalize(const teal_step_plan& P, const teal_step_g
         case TEAL_SEPI_RESID: {
             float xn = 0.f;
             if (col < g.n) {
-                xn = __ldcg(g.resid + col) + v;
+                xn = pre + v;
                 g.resid[col] = xn;
             }
             const float ss = block_sum_nt(xn * xn, s);
@@ -394,20 +405,32 @@ __device__ __forceinline__ int owner_of(int64_t gidx, int64_t F, int G) {
 }
 
 // Threshold + compact rows [r0, r1) of one tile into s.u.g (ordered).
+// `rden` < 0: compute the RMSNorm denominator here (warp 0), its
+// sum-of-squares loads in flight together with every thread's x / gain loads.
 __device__ int compact_rows(const teal_step_group& g, const teal_step_tile& tm, int tile, int r0, int r1,
-                            float rden, bool rms, Smem& s) {
+                            float& rden, bool rms, Smem& s) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool two = tm.seg_hi != tm.seg_lo;
     constexpr int RPT = MAXR / NT;  // rows per thread
-    float hx[RPT];
+    float hx[RPT], gx[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {  // all x (and gain) loads in flight at once
         const int i = r0 + q * NT + tid;
         hx[q] = 0.f;
+        gx[q] = 1.f;
         if (i < r1) {
-            const float xv = __ldcg(g.x + i);
-            hx[q] = rms ? (xv / rden) * __ldg(g.gain + i) : xv;
+            hx[q] = __ldcg(g.x + i);
+            if (rms) gx[q] = __ldg(g.gain + i);
         }
+    }
+    if (rms) {
+        if (rden < 0.f) {
+            if (warp == 0) s.rden = rms_den(g, lane);
+            __syncthreads();
+            rden = s.rden;
+        }
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) hx[q] = (hx[q] / rden) * gx[q];
     }
     int base = 0;
 #pragma unroll 1
@@ -604,12 +627,7 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
         }
     }
     if (ph.dep_kind == TEAL_DEP_GLOBAL) wait_range(P.counters, ph.dep, ph.dep, ph.target);
-    float rden = 1.f;
-    if (rms) {
-        if (warp == 0) s.rden = rms_den(g, lane);
-        __syncthreads();
-        rden = s.rden;
-    }
+    float rden = rms ? -1.f : 1.f;  // computed by the first compaction, overlapped with its x loads
     constexpr int ROWB = WFmt<WT>::ROWB;
     int segi = 0, lasts = 0;
 #define SL_STAMP(k, v) do { if (tl && tid == 0) tl[k] = (v); } while (0)
@@ -658,6 +676,8 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
         for (int w = 0; w < NW; ++w) v += s.red[w * TW + tid];
         const int cf = owner_of((int64_t)tile * gpt, F, G);
         const int cl = owner_of((int64_t)(tile + 1) * gpt - 1, F, G);
+        const bool resid = g.epilogue == TEAL_SEPI_RESID && (int64_t)tile * TW + tid < g.n;
+        float pre = 0.f;
         if (cl > cf) {
             float* slot = g.partials + ((int64_t)tile * g.maxc + (c - cf)) * TW;
             __stcg(slot + tid, v);
@@ -665,6 +685,7 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
                 if (segi == 0) SL_STAMP(4, gtimer());
                 continue;
             }
+            if (resid) pre = __ldcg(g.resid + (int64_t)tile * TW + tid);  // in flight with the partials
             const float* pb = g.partials + (int64_t)tile * g.maxc * TW + tid;
             const int nc = cl - cf + 1;
             v = 0.f;
@@ -677,8 +698,11 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
                     if (s0 + q < nc) v += pv[q];
             }
         }
+        else if (resid) {
+            pre = __ldcg(g.resid + (int64_t)tile * TW + tid);
+        }
         if (g.col_scale) v *= g.col_scale[(int64_t)tile * TW + tid];
-        finalize(P, g, tile, v, s);
+        finalize(P, g, tile, v, s, pre);
         ++lasts;
         if (segi == 0) SL_STAMP(4, gtimer());
     }
