@@ -251,6 +251,17 @@ int teal_argmax(const float* logits, int64_t n, int* out_token,
 #define TEAL_PHASE_LOAD 0
 #define TEAL_PHASE_GEMV 1
 #define TEAL_PHASE_ATTN 2
+#define TEAL_PHASE_RESID 3   /* x_out = x + fx(in_acc), CTA-partitioned (plans without an LM head) */
+/* Step-engine prologues reading a fixed-point accumulator (see ACC below) */
+#define TEAL_PRO_RMS_ACC 2   /* x' = x + fx(in_acc); h = RMSNorm(x'); each CTA writes its share of x' to x_out */
+#define TEAL_PRO_SILU_ACC 3  /* h_i = silu(fx(in_acc[gate_i])) * fx(in_acc[up_i]) (gate/up tile layout) */
+/* ACC output (group.acc != NULL): every split-K contributor adds its column
+ * partials to an int64 fixed-point accumulator (2^-TEAL_STEP_FX_BITS units,
+ * integer addition: order-independent, so deterministic) and bumps the
+ * tile's counters so that each finished tile adds TEAL_STEP_CONTRIB in total.
+ * Range |value| < 2^31. */
+#define TEAL_STEP_FX_BITS 32
+#define TEAL_STEP_CONTRIB 1024
 #define TEAL_DEP_NONE 0
 #define TEAL_DEP_GLOBAL 1    /* counters[dep] >= target                          */
 #define TEAL_DEP_ROWS 2      /* counters[dep + r / dep_rows] >= target for every input row r read */
@@ -301,6 +312,9 @@ typedef struct teal_step_group {
     float t_all;             /* tiles == NULL: one threshold for every tile  */
     int64_t tile_stride_b;   /* row_stride_b == 0: tiled (m*TW*esz, TW*esz)   */
     int64_t row_stride_b;    /* else untiled input-major: TW*esz, ldw*esz    */
+    long long* acc;          /* nullable ACC output [ntiles*TW] (zero at step start) */
+    const long long* in_acc; /* PRO_RMS_ACC: delta [m]; PRO_SILU_ACC: gate/up accumulator */
+    float* x_out;            /* PRO_RMS_ACC / PHASE_RESID: materialised x' [m]  */
 } teal_step_group;
 
 typedef struct teal_step_attn {
@@ -348,6 +362,8 @@ typedef struct teal_step_plan {
     int pad_;
     int d, emb_dtype;
     int w_dtype, ctas;               /* ctas: grid size (<= resident capacity)  */
+    long long* acc_zero;             /* LOAD: ACC accumulators zeroed each step */
+    int64_t acc_zero_n;              /* (elements)                              */
 } teal_step_plan;
 
 /* Resident CTAs per SM of the step kernel for a weight dtype; the plan's

@@ -54,6 +54,8 @@ constexpr int ATT_MAXHD = 128;
 constexpr int ATT_MAXCHUNK = 256;
 constexpr int ATT_STAGE = 16384;  // bytes of K (and of V) staged per attention unit
 constexpr int ATT_MAXCHUNK_STAGE = 128;  // staged positions (>= 16384 / (hd * kv bytes))
+constexpr int XS_MAX = 8192;      // PRO_RMS_ACC: the CTA's copy of x' (m <= XS_MAX)
+constexpr int CONTRIB = TEAL_STEP_CONTRIB;
 static_assert(NT == TW, "epilogues map one thread per tile column");
 
 struct Smem {
@@ -62,6 +64,7 @@ struct Smem {
             int idx[MAXR];    // row - r0 | keep_lo << 30 | keep_hi << 31
             float h[MAXR];
             float gsc[GSC_MAX * TW];  // int4: scales of the chunk's row groups
+            float xs[XS_MAX];         // PRO_RMS_ACC: x' = x + fx(in_acc), all m channels
         } g;
         struct {
             float q[ATT_MAXG * ATT_MAXHD];
@@ -120,10 +123,21 @@ __device__ __forceinline__ unsigned atom_acq_rel_add(unsigned* p, unsigned v) {
     return old;
 }
 
-__device__ __forceinline__ void signal(int* counters, int c0, int c1) {
+__device__ __forceinline__ void signal(int* counters, int c0, int c1, int w = 1) {
     __syncthreads();
     if (threadIdx.x == 0 && c0 >= 0)
-        for (int c = c0; c <= c1; ++c) red_release(counters + (int64_t)c * CSTRIDE, 1);
+        for (int c = c0; c <= c1; ++c) red_release(counters + (int64_t)c * CSTRIDE, w);
+}
+
+// ---- fixed-point accumulators (ACC outputs) ---------------------------------
+// Split-K contributors add int64 multiples of 2^-32 instead of handing fp32
+// partials to a last arriver: integer addition is associative, so the sum is
+// the same whatever order the contributors arrive in (deterministic), and no
+// contributor waits for another — the reduction leaves the critical path.
+__device__ __forceinline__ long long to_fx(float v) { return __float2ll_rn(v * 4294967296.0f); }
+__device__ __forceinline__ float from_fx(long long a) { return __ll2float_rn(a) * 2.3283064365386963e-10f; }
+__device__ __forceinline__ void red_add_s64(long long* p, long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // Take a split-K ticket after storing this CTA's partial: returns (to every
@@ -387,6 +401,43 @@ __device__ __forceinline__ float rms_den(const teal_step_group& g, int lane) {
     return sqrtf(a / (float)g.m + g.eps);
 }
 
+// PRO_RMS_ACC: x' = x + fx(in_acc) over all m channels into s.u.g.xs (every
+// load in flight at once), CTA c of G writes its share [c*m/G, (c+1)*m/G) of
+// x' to x_out (the next residual version), and returns the RMSNorm
+// denominator.  Every CTA computes the same sum in the same order, so all
+// tiles threshold the same h.
+__device__ float rms_acc_prep(const teal_step_group& g, int c, int G, Smem& s) {
+    const int tid = threadIdx.x, m = g.m;
+    const int p0 = (int)((int64_t)c * m / G), p1 = (int)((int64_t)(c + 1) * m / G);
+    float ss = 0.f;
+#pragma unroll 1
+    for (int i0 = 0; i0 < m; i0 += 16 * NT) {
+        float xb[16];
+        long long xa[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int i = i0 + q * NT + tid;
+            xb[q] = 0.f;
+            xa[q] = 0;
+            if (i < m) {
+                xb[q] = __ldcg(g.x + i);
+                xa[q] = __ldcg(g.in_acc + i);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int i = i0 + q * NT + tid;
+            if (i < m) {
+                const float xn = xb[q] + from_fx(xa[q]);
+                s.u.g.xs[i] = xn;
+                ss = fmaf(xn, xn, ss);
+                if (i >= p0 && i < p1) g.x_out[i] = xn;
+            }
+        }
+    }
+    return sqrtf(block_sum_nt(ss, s) / (float)m + g.eps);
+}
+
 // CTAs taking part in a GEMV phase: never more than the 32-row groups (every
 // range non-empty) and, when the phase has at most half as many tiles as the
 // grid has CTAs, a multiple of the tile count so that every range lies inside
@@ -413,14 +464,33 @@ __device__ int compact_rows(const teal_step_group& g, const teal_step_tile& tm, 
     const bool two = tm.seg_hi != tm.seg_lo;
     constexpr int RPT = MAXR / NT;  // rows per thread
     float hx[RPT], gx[RPT];
+    if (g.prologue == TEAL_PRO_SILU_ACC) {  // h = silu(gate) * up from the gate/up accumulator
+        long long ga[RPT], ua[RPT];
 #pragma unroll
-    for (int q = 0; q < RPT; ++q) {  // all x (and gain) loads in flight at once
-        const int i = r0 + q * NT + tid;
-        hx[q] = 0.f;
-        gx[q] = 1.f;
-        if (i < r1) {
-            hx[q] = __ldcg(g.x + i);
-            if (rms) gx[q] = __ldg(g.gain + i);
+        for (int q = 0; q < RPT; ++q) {
+            const int i = r0 + q * NT + tid;
+            ga[q] = ua[q] = 0;
+            if (i < r1) {
+                const int64_t b = (int64_t)(i / TH) * TW + (i % TH);
+                ga[q] = __ldcg(g.in_acc + b);
+                ua[q] = __ldcg(g.in_acc + b + TH);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            hx[q] = silu(from_fx(ga[q])) * from_fx(ua[q]);
+            gx[q] = 1.f;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {  // all x (and gain) loads in flight at once
+            const int i = r0 + q * NT + tid;
+            hx[q] = 0.f;
+            gx[q] = 1.f;
+            if (i < r1) {
+                hx[q] = g.prologue == TEAL_PRO_RMS_ACC ? s.u.g.xs[i] : __ldcg(g.x + i);
+                if (rms) gx[q] = __ldg(g.gain + i);
+            }
         }
     }
     if (rms) {
@@ -610,7 +680,7 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
     const int G = participants(g.ntiles, F), c = blockIdx.x;
     if (c >= G) return;
     const int64_t g0 = (int64_t)c * F / G, g1 = (int64_t)(c + 1) * F / G;
-    const bool rms = g.prologue == TEAL_PRO_RMSNORM;
+    const bool rms = g.prologue == TEAL_PRO_RMSNORM || g.prologue == TEAL_PRO_RMS_ACC;
     // While this slice waits for its inputs, pull the head of its weight range
     // into L2 (one bulk prefetch of contiguous tiled rows): the wait is tail
     // time of the previous phase, when HBM is mostly idle.  Rows that turn out
@@ -627,7 +697,9 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
         }
     }
     if (ph.dep_kind == TEAL_DEP_GLOBAL) wait_range(P.counters, ph.dep, ph.dep, ph.target);
-    float rden = rms ? -1.f : 1.f;  // computed by the first compaction, overlapped with its x loads
+    // PRO_RMSNORM: rden computed by the first compaction, overlapped with its x loads
+    float rden = rms ? -1.f : 1.f;
+    if (g.prologue == TEAL_PRO_RMS_ACC) rden = rms_acc_prep(g, c, G, s);
     constexpr int ROWB = WFmt<WT>::ROWB;
     int segi = 0, lasts = 0;
 #define SL_STAMP(k, v) do { if (tl && tid == 0) tl[k] = (v); } while (0)
@@ -676,6 +748,14 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
         for (int w = 0; w < NW; ++w) v += s.red[w * TW + tid];
         const int cf = owner_of((int64_t)tile * gpt, F, G);
         const int cl = owner_of((int64_t)(tile + 1) * gpt - 1, F, G);
+        if (g.acc) {  // ACC output: add this CTA's partial, bump the counters by its share of CONTRIB
+            if (g.col_scale) v *= g.col_scale[(int64_t)tile * TW + tid];
+            red_add_s64(g.acc + (int64_t)tile * TW + tid, to_fx(v));
+            signal(P.counters, tm.sig0, tm.sig1, c == cf ? CONTRIB - (cl - cf) : 1);
+            ++lasts;
+            if (segi == 0) SL_STAMP(4, gtimer());
+            continue;
+        }
         const bool resid = g.epilogue == TEAL_SEPI_RESID && (int64_t)tile * TW + tid < g.n;
         float pre = 0.f;
         if (cl > cf) {
@@ -922,7 +1002,7 @@ __device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, S
     const teal_step_attn& a = P.attns[ph.group];
     // the sequence length is written by this step's load phase: a CTA that had
     // no qkv slice reaches this point without having waited for it
-    wait_range(P.counters, 0, 0, 1);
+    wait_range(P.counters, 0, 0, (int)gridDim.x);
     const int L = __ldcg(P.state + 1);
     const int nact = min(a.nchunks, (L + a.chunk - 1) / a.chunk);  // chunks holding positions
     const int nu = a.KVH * nact;
@@ -941,8 +1021,16 @@ __device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, S
 
 // ---- residual load: x = emb[token] (or x_in); ss partials; {pos, len} ---------
 __device__ __noinline__ void load_phase(const teal_step_plan& P, Smem& s) {
-    if (blockIdx.x != 0) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (P.acc_zero) {  // every CTA zeroes its share of this step's ACC accumulators (16 B stores)
+        int4* z = reinterpret_cast<int4*>(P.acc_zero);
+        const int64_t n2 = P.acc_zero_n >> 1;
+        for (int64_t i = (int64_t)blockIdx.x * NT + tid; i < n2; i += (int64_t)gridDim.x * NT) z[i] = make_int4(0, 0, 0, 0);
+    }
+    if (blockIdx.x != 0) {
+        signal(P.counters, 0, 0);
+        return;
+    }
     if (tid == 0) {
         const int len = P.state[1];
         P.state[0] = len;
@@ -985,6 +1073,13 @@ __device__ __noinline__ void load_phase(const teal_step_plan& P, Smem& s) {
     signal(P.counters, 0, 0);
 }
 
+// ---- residual materialisation (plans without an LM head) --------------------
+__device__ void resid_phase(const teal_step_plan& P, const teal_step_phase& ph, const teal_step_group& g) {
+    wait_range(P.counters, ph.dep, ph.dep, ph.target);
+    for (int i = blockIdx.x * NT + threadIdx.x; i < g.m; i += gridDim.x * NT)
+        g.x_out[i] = __ldcg(g.x + i) + from_fx(__ldcg(g.in_acc + i));
+}
+
 // MINB resident CTAs per SM (register budget 65536 / (NT * MINB)); UB rows in
 // flight per warp per pipeline stage.
 template <int WT, int MINB, int UB>
@@ -999,6 +1094,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const __grid_constant__ 
         if (tl && tid == 0) tl[0] = gtimer();
         if (ph.kind == TEAL_PHASE_GEMV) gemv_slice_t<WT, UB>(P, ph, P.groups[ph.group], s, pol, tl);
         else if (ph.kind == TEAL_PHASE_ATTN) attn_phase(P, ph, s);
+        else if (ph.kind == TEAL_PHASE_RESID) resid_phase(P, ph, P.groups[ph.group]);
         else load_phase(P, s);
         __syncthreads();
         if (tl && tid == 0) tl[1] = gtimer();
@@ -1193,6 +1289,8 @@ int teal_step_launch(const teal_step_plan* p, cudaStream_t stream) {
     TEAL_REQUIRE(p && p->groups && p->phases && p->counters && p->ctrl && p->x && p->ss && p->state,
                  "teal_step_launch: null plan field");
     TEAL_REQUIRE(p->nphases >= 1 && p->ncounters >= 1, "teal_step_launch: empty plan");
+    TEAL_REQUIRE(!p->acc_zero || (p->acc_zero_n % 2 == 0 && (reinterpret_cast<uintptr_t>(p->acc_zero) & 15) == 0),
+                 "teal_step_launch: acc_zero must be 16-byte aligned with an even element count");
     TEAL_REQUIRE(p->d >= TW && p->d % TW == 0, "teal_step_launch: d must be a multiple of %d", TW);
     TEAL_REQUIRE(p->w_dtype == TEAL_BF16 || p->w_dtype == TEAL_F32 || p->w_dtype == TEAL_I8 || p->w_dtype == TEAL_I4,
                  "teal_step_launch: weights must be bf16, fp32, int8 or int4");

@@ -48,7 +48,8 @@ class StepGroup(ctypes.Structure):
                 ("max_seq", c_i64), ("m", c_i), ("n", c_i), ("ntiles", c_i), ("maxc", c_i),
                 ("prologue", c_i), ("nss", c_i), ("eps", c_f), ("epilogue", c_i),
                 ("nq", c_i), ("nkv", c_i), ("head_dim", c_i), ("kv_dtype", c_i), ("w_dtype", c_i),
-                ("gscale", c_vp), ("group", c_i), ("t_all", c_f), ("tile_stride_b", c_i64), ("row_stride_b", c_i64)]
+                ("gscale", c_vp), ("group", c_i), ("t_all", c_f), ("tile_stride_b", c_i64), ("row_stride_b", c_i64),
+                ("acc", c_vp), ("in_acc", c_vp), ("x_out", c_vp)]
 
 
 class StepAttn(ctypes.Structure):
@@ -67,10 +68,14 @@ class StepPlan(ctypes.Structure):
                 ("emb", c_vp), ("x_in", c_vp), ("token", c_vp), ("x", c_vp), ("ss", c_vp), ("state", c_vp),
                 ("cand_v", c_vp), ("cand_i", c_vp), ("token_out", c_vp), ("lm_done", c_vp), ("timeline", c_vp),
                 ("nphases", c_i), ("ncounters", c_i), ("prefetch_bytes", c_i), ("pad_", c_i),
-                ("d", c_i), ("emb_dtype", c_i), ("w_dtype", c_i), ("ctas", c_i)]
+                ("d", c_i), ("emb_dtype", c_i), ("w_dtype", c_i), ("ctas", c_i),
+                ("acc_zero", c_vp), ("acc_zero_n", c_i64)]
 
 
-PHASE_LOAD, PHASE_GEMV, PHASE_ATTN = 0, 1, 2
+PHASE_LOAD, PHASE_GEMV, PHASE_ATTN, PHASE_RESID = 0, 1, 2, 3
+PRO_RMS_ACC, PRO_SILU_ACC = 2, 3
+CONTRIB = 1024  # TEAL_STEP_CONTRIB: counter units per finished tile of an ACC output
+XS_MAX = 8192   # PRO_RMS_ACC staging limit on d
 DEP_NONE, DEP_GLOBAL, DEP_ROWS = 0, 1, 2
 
 
@@ -300,6 +305,8 @@ class StepDecoder:
         G = spec.n_heads // spec.n_kv_heads
         if d % TW or nq % TW or nkv % TW or TW % hd or f % TH:
             raise ValueError(f"StepDecoder needs d, n_q, n_kv multiples of {TW}, head_dim | {TW}, d_ff multiple of {TH}")
+        if d > XS_MAX:
+            raise ValueError(f"StepDecoder needs d_model <= {XS_MAX}")
         if G > 8 or hd > 128 or G * hd > 1024:
             raise ValueError("StepDecoder attention supports <= 8 q heads per kv head and head_dim <= 128")
         kvb = torch.empty(0, dtype=kv_dtype or weights.dtype).element_size()
@@ -325,7 +332,10 @@ class StepDecoder:
             self.lm_t = quantize_tiles(pack_tiled(weights.lm_head), quant) if spec.vocab else None
         self.w_code = (self.tw[0]["qkv"].dtype_code if self.tw else RT.dtype_code(weights.dtype))
         # activations / state
-        self.x = torch.zeros(d, **f32)
+        # residual stream versions: xv[0] the loaded row, xv[2l+1] after layer
+        # l's attention, xv[2l+2] after its MLP; x = xv[2L] the step's output
+        self.xv = torch.zeros(2 * L + 1, d, **f32)
+        self.x = self.xv[2 * L]
         self.x_in = torch.zeros(d, **f32)
         self.ss = torch.zeros(d // TW, **f32)
         self.q = torch.zeros(nq, **f32)
@@ -396,6 +406,15 @@ class StepDecoder:
                    for k in ("qkv", "o", "gu", "down", "lm", "attn")}
         rec = G * hd + 2 * G
         self.ws["attn"] = torch.zeros(KVH * self.nchunks * rec, device=dev)
+        # ACC accumulators per layer (int64 fixed point, zeroed by every step's
+        # load phase): o and down deltas of the residual [d], gate/up [nt_gu*TW]
+        per_acc = 2 * d + nt_gu * TW
+        self.acc = torch.zeros(L * per_acc, device=dev, dtype=torch.int64)
+
+        def accs(l):
+            b = self.acc[l * per_acc:(l + 1) * per_acc]
+            return dict(o=b[:d], down=b[d:2 * d], gu=b[2 * d:])
+        K_ = CONTRIB
 
         groups, attns, phases, keep = [], [], [], []
         T, K = self.taps, self.kept
@@ -414,7 +433,13 @@ class StepDecoder:
             tw = self.tw[l]
             lw = self.w.layers[l]
             kc, vc = self.kcache[l], self.vcache[l]
-            dep_in = (0, 1) if l == 0 else (cbase(l - 1)["down"], nt_dn)
+            A = accs(l)
+            if l == 0:  # the loaded row (sum-of-squares partials from the load phase)
+                dep_in, qkv_in = (0, Gc), dict(x=self.xv[0], prologue=C.PRO_RMSNORM)
+            else:       # x' = previous version + previous layer's down accumulator
+                dep_in = (cbase(l - 1)["down"], nt_dn * K_)
+                qkv_in = dict(x=self.xv[2 * l - 1], prologue=PRO_RMS_ACC, in_acc=accs(l - 1)["down"],
+                              x_out=self.xv[2 * l])
             # --- qkv: RMSNorm(x) -> 3 thresholds -> q (RoPE), k (RoPE) -> cache, v -> cache
             meta, feeds = [], [0] * KVH
             for ti in range(nt_qkv):
@@ -431,7 +456,7 @@ class StepDecoder:
                 tv = _t32(t[seg])
                 meta.append(StepTile(tv, tv, seg, seg, int(first), int(first), cb["attn"] + g0, cb["attn"] + g1))
             groups.append(self._group(tw["qkv"], tiles_tensor(meta), m=d, n=nq + 2 * nkv, maxc=mc["qkv"],
-                                      x=self.x, gain=lw.rms_attn, prologue=C.PRO_RMSNORM, ws="qkv",
+                                      gain=lw.rms_attn, ws="qkv", **qkv_in,
                                       epilogue=SEPI_QKV, q_out=self.q, k_cache=kc, v_cache=vc,
                                       dbg=(T.h["pre_attn"][l] if T else None,
                                            [T.bits[p][l] for p in ("q", "k", "v")] if T else None,
@@ -449,7 +474,7 @@ class StepDecoder:
             tv = _t32(t[3])
             meta = [StepTile(tv, tv, 0, 0, int(ti == 0), int(ti == 0), cb["odone"], cb["odone"]) for ti in range(nt_o)]
             groups.append(self._group(tw["o"], tiles_tensor(meta), m=nq, n=d, maxc=mc["o"], x=self.ctx,
-                                      prologue=C.PRO_PLAIN, ws="o", epilogue=SEPI_RESID,
+                                      prologue=C.PRO_PLAIN, ws="o", epilogue=SEPI_RESID, acc=A["o"],
                                       dbg=(T.h["attn_out"][l] if T else None, [T.bits["o"][l]] if T else None,
                                            [K[l, 3]] if K is not None else None)))
             phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_ROWS, cb["odep"], 1, G * hd))
@@ -457,33 +482,41 @@ class StepDecoder:
             tg, tu = _t32(t[4]), _t32(t[5])
             meta = [StepTile(tg, tu, 0, 1, int(ti == 0), int(ti == 0), cb["gu"] + ti, cb["gu"] + ti)
                     for ti in range(nt_gu)]
-            groups.append(self._group(tw["gu"], tiles_tensor(meta), m=d, n=f, maxc=mc["gu"], x=self.x,
-                                      gain=lw.rms_mlp, prologue=C.PRO_RMSNORM, ws="gu", epilogue=SEPI_SILU,
+            groups.append(self._group(tw["gu"], tiles_tensor(meta), m=d, n=f, maxc=mc["gu"], x=self.xv[2 * l],
+                                      gain=lw.rms_mlp, prologue=PRO_RMS_ACC, in_acc=A["o"], x_out=self.xv[2 * l + 1],
+                                      ws="gu", epilogue=SEPI_SILU, acc=A["gu"],
                                       dbg=(T.h["pre_mlp"][l] if T else None,
                                            [T.bits["gate"][l], T.bits["up"][l]] if T else None,
                                            [K[l, 4], K[l, 5]] if K is not None else None)))
-            phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_GLOBAL, cb["odone"], nt_o, 1))
+            phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_GLOBAL, cb["odone"], nt_o * K_, 1))
             # --- down: rows = intermediate channels, each waits for its gate/up tile
             tv = _t32(t[6])
             meta = [StepTile(tv, tv, 0, 0, int(ti == 0), int(ti == 0), cb["down"], cb["down"]) for ti in range(nt_dn)]
             groups.append(self._group(tw["down"], tiles_tensor(meta), m=f, n=d, maxc=mc["down"], x=self.inter,
-                                      prologue=C.PRO_PLAIN, ws="down", epilogue=SEPI_RESID,
+                                      prologue=PRO_SILU_ACC, in_acc=A["gu"], ws="down", epilogue=SEPI_RESID,
+                                      acc=A["down"],
                                       dbg=(T.h["mlp_inter"][l] if T else None, [T.bits["down"][l]] if T else None,
                                            [K[l, 6]] if K is not None else None)))
-            phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_ROWS, cb["gu"], 1, TH))
+            phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_ROWS, cb["gu"], K_, TH))
         if spec.vocab:
             nt_lm = self.lm_t.ntiles
             mc_lm = max_contributors(nt_lm, d, Gc)
             self.ws["lm"] = torch.zeros(nt_lm * mc_lm * TW, device=dev)
             self.tk["lm"] = torch.zeros(max(4096, nt_lm), device=dev, dtype=torch.int32)
             meta = [StepTile(float("-inf"), float("-inf"), 0, 0, 0, 0, -1, -1) for _ in range(nt_lm)]
-            groups.append(self._group(self.lm_t, tiles_tensor(meta), m=d, n=spec.vocab, maxc=mc_lm, x=self.x,
-                                      gain=self.w.final_norm, prologue=C.PRO_RMSNORM, ws="lm",
+            groups.append(self._group(self.lm_t, tiles_tensor(meta), m=d, n=spec.vocab, maxc=mc_lm,
+                                      x=self.xv[2 * L - 1], gain=self.w.final_norm, prologue=PRO_RMS_ACC,
+                                      in_acc=accs(L - 1)["down"], x_out=self.xv[2 * L], ws="lm",
                                       epilogue=SEPI_LOGITS, y=self.logits))
-            phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_GLOBAL, cbase(L - 1)["down"], nt_dn, 1))
+            phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_GLOBAL, cbase(L - 1)["down"], nt_dn * K_, 1))
             self.cand_v = torch.zeros(nt_lm, device=dev)
             self.cand_i = torch.zeros(nt_lm, device=dev, dtype=torch.int32)
-        else:
+        else:  # no LM head: materialise the output row x = xv[2L]
+            g = StepGroup()
+            g.x, g.in_acc, g.x_out, g.m = self.xv[2 * L - 1].data_ptr(), accs(L - 1)["down"].data_ptr(), \
+                self.xv[2 * L].data_ptr(), d
+            groups.append(g)
+            phases.append(StepPhase(PHASE_RESID, len(groups) - 1, DEP_GLOBAL, cbase(L - 1)["down"], nt_dn * K_, 1))
             self.cand_v = torch.zeros(1, device=dev)
             self.cand_i = torch.zeros(1, device=dev, dtype=torch.int32)
         self.lm_done = torch.zeros(1, device=dev, dtype=torch.int32)
@@ -500,7 +533,8 @@ class StepDecoder:
         p.counters, p.ctrl = self.counters.data_ptr(), self.ctrl.data_ptr()
         if spec.vocab:
             p.emb, p.emb_dtype = self.w.embedding.data_ptr(), RT.dtype_code(self.w.embedding.dtype)
-        p.x_in, p.token, p.x, p.ss, p.state = (self.x_in.data_ptr(), self.token.data_ptr(), self.x.data_ptr(),
+        p.acc_zero, p.acc_zero_n = self.acc.data_ptr(), self.acc.numel()
+        p.x_in, p.token, p.x, p.ss, p.state = (self.x_in.data_ptr(), self.token.data_ptr(), self.xv[0].data_ptr(),
                                                self.ss.data_ptr(), self.state.data_ptr())
         p.cand_v, p.cand_i, p.token_out, p.lm_done = (self.cand_v.data_ptr(), self.cand_i.data_ptr(),
                                                       self.token.data_ptr(), self.lm_done.data_ptr())
@@ -519,7 +553,7 @@ class StepDecoder:
         return self.timeline
 
     def _group(self, wt, tiles, m, n, maxc, x, prologue, ws, epilogue, gain=None, q_out=None, k_cache=None,
-               v_cache=None, y=None, dbg=None):
+               v_cache=None, y=None, dbg=None, acc=None, in_acc=None, x_out=None):
         spec = self.spec
         g = StepGroup()
         g.w, g.tiles, g.x = wt.data.data_ptr(), tiles.data_ptr(), x.data_ptr()
@@ -544,6 +578,7 @@ class StepDecoder:
         g.prologue, g.nss, g.eps, g.epilogue = prologue, spec.d_model // TW, spec.norm_eps, epilogue
         g.nq, g.nkv, g.head_dim, g.kv_dtype = spec.n_q, spec.n_kv, spec.head_dim, RT.dtype_code(self.kv_dtype)
         g.w_dtype = wt.dtype_code
+        g.acc, g.in_acc, g.x_out = RT.ptr(acc), RT.ptr(in_acc), RT.ptr(x_out)
         return g
 
     # -- step -----------------------------------------------------------------
