@@ -331,6 +331,12 @@ typedef struct teal_step_attn {
     int dep_base;            /* unit (g, *) waits for counters[dep_base + g] >= dep_target[g] */
     const int* dep_target;   /* [KVH]                                         */
     unsigned long long* dbg; /* nullable debug: [KVH*nchunks][6] %globaltimer stamps */
+    const long long* qkv_acc;  /* nullable: q|k|v ACC accumulator of the qkv group; the
+                                  units then apply RoPE themselves and the unit holding
+                                  the new position writes its k, v to the cache */
+    const float* rope_cos;   /* nullable [max_seq][hd/2]                      */
+    const float* rope_sin;
+    int nq, nkv;             /* q / k columns (qkv_acc offsets)               */
 } teal_step_attn;
 
 typedef struct teal_step_phase {

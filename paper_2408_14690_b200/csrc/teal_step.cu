@@ -794,16 +794,113 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
 // One kernel instantiation per weight format: every GEMV group of a plan
 // (layers and LM head) uses the plan's w_dtype.
 
+// Stage one attention unit's inputs in shared memory: q of kv group g
+// (from the plan's q vector, or from the qkv accumulator with RoPE applied)
+// and the chunk's np K / V rows from the cache.  With the accumulator, the
+// row of the step's new position (newrow >= 0) is built from it instead: k
+// (RoPE) and v, also written to the cache.  Every load of the thread is in
+// flight before any is consumed (one L2 round trip).
+template <typename KT>
+__device__ __noinline__ void attn_stage(const teal_step_attn& a, int g, int p0, int np, int pos, int newrow,
+                                        int64_t kvbase, Smem& s) {
+    constexpr int KB = (int)sizeof(KT);
+    constexpr int QPT = ATT_MAXG * ATT_MAXHD / NT;
+    constexpr int PER = ATT_STAGE / 16 / NT;  // n16 <= ATT_STAGE / 16 = PER * NT
+    const int tid = threadIdx.x, G = a.H / a.KVH, hd = a.hd, half = hd >> 1;
+    const int n16 = np * hd * KB / 16;
+    const int vpr = hd * KB / 16;  // 16-byte vectors per K/V row
+    const uint4* gk = reinterpret_cast<const uint4*>(reinterpret_cast<const KT*>(a.k_cache) + kvbase + (int64_t)p0 * hd);
+    const uint4* gv = reinterpret_cast<const uint4*>(reinterpret_cast<const KT*>(a.v_cache) + kvbase + (int64_t)p0 * hd);
+    const bool acc = a.qkv_acc != nullptr;
+    // NT is a multiple of hd: every element this thread touches (q heads and
+    // the new k) has head dim d = tid % hd, so one RoPE pair serves all
+    const int d = tid % hd, dd = d < half ? d : d - half;
+    const int part = d < half ? half : -half;
+    const bool rope = acc && a.rope_cos;
+    long long qa[QPT], qp[QPT], ka = 0, kp = 0, va = 0;
+    float qf[QPT];
+    float cs = 1.f, sn = 0.f;
+    if (rope) {
+        cs = __ldg(a.rope_cos + (int64_t)pos * half + dd);
+        sn = __ldg(a.rope_sin + (int64_t)pos * half + dd);
+    }
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) {
+        const int o = tid + j * NT;
+        const int64_t qc = (int64_t)g * G * hd + o;
+        qa[j] = qp[j] = 0;
+        qf[j] = 0.f;
+        if (o < G * hd) {
+            if (!acc) {
+                qf[j] = __ldcg(a.q + qc);
+            } else {
+                qa[j] = __ldcg(a.qkv_acc + qc);
+                if (rope) qp[j] = __ldcg(a.qkv_acc + qc + part);
+            }
+        }
+    }
+    const bool nk = newrow >= 0 && tid < hd;
+    const int64_t kc = (int64_t)a.nq + (int64_t)g * hd + tid;
+    if (nk) {
+        ka = __ldcg(a.qkv_acc + kc);
+        if (rope) kp = __ldcg(a.qkv_acc + kc + part);
+        va = __ldcg(a.qkv_acc + kc + a.nkv);
+    }
+    uint4 kk[PER], vv[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int v = tid + q * NT;
+        if (v < n16 && v / vpr != newrow) { kk[q] = __ldcg(gk + v); vv[q] = __ldcg(gv + v); }
+    }
+    const float sgn = d < half ? -1.f : 1.f;  // x*cos -/+ partner*sin
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) {
+        const int o = tid + j * NT;
+        if (o < G * hd) {
+            float r = qf[j];
+            if (acc) r = rope ? fmaf(sgn * from_fx(qp[j]), sn, from_fx(qa[j]) * cs) : from_fx(qa[j]);
+            s.u.a.q[o] = r;
+        }
+    }
+    if (nk) {
+        const float kr = rope ? fmaf(sgn * from_fx(kp), sn, from_fx(ka) * cs) : from_fx(ka);
+        const float vr = from_fx(va);
+        const int64_t off = kvbase + (int64_t)pos * hd + d;
+        KT* kst = reinterpret_cast<KT*>(s.u.a.k) + (int64_t)newrow * (vpr + 4) * (16 / KB) + d;
+        KT* vst = reinterpret_cast<KT*>(s.u.a.v) + (int64_t)newrow * hd + d;
+        if constexpr (KB == 2) {
+            const uint16_t kb = f32_to_bf16_rn(kr), vb = f32_to_bf16_rn(vr);
+            reinterpret_cast<uint16_t*>(const_cast<void*>(a.k_cache))[off] = kb;
+            reinterpret_cast<uint16_t*>(const_cast<void*>(a.v_cache))[off] = vb;
+            *kst = kb;
+            *vst = vb;
+        } else {
+            reinterpret_cast<float*>(const_cast<void*>(a.k_cache))[off] = kr;
+            reinterpret_cast<float*>(const_cast<void*>(a.v_cache))[off] = vr;
+            *kst = kr;
+            *vst = vr;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int v = tid + q * NT;
+        if (v < n16 && v / vpr != newrow) {
+            s.u.a.k[(v / vpr) * (vpr + 4) + v % vpr] = kk[q];  // K row p at p*(vpr+4) (64-B pad)
+            s.u.a.v[v] = vv[q];
+        }
+    }
+}
+
 // ---- attention unit: (kv head g, position chunk) -------------------------------
 // Deliberately compact code (runtime loops over heads and head_dim chunks):
 // this path runs on a few CTAs once per layer, so its instructions are cold
 // in the instruction cache every time; unrolled code here costs more in
 // instruction fetch than it saves in issue slots.
 template <typename KT>
-__device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_step_attn& a, int g, int ch, Smem& s) {
+__device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_step_attn& a, int g, int ch, int L,
+                                        Smem& s) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = a.H / a.KVH, hd = a.hd;
-    const int L = __ldcg(P.state + 1);
     const int p0 = ch * a.chunk;
     const int p1 = min(L, p0 + a.chunk);
     const int np = max(0, p1 - p0);
@@ -814,32 +911,13 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
 #define ATT_STAMP(k) do { if (dbg && tid == 0) dbg[k] = gtimer(); } while (0)
     ATT_STAMP(0);
     if (np > 0) {
-        // stage q, and the chunk's K and V rows (contiguous in the cache), with
-        // 16-byte loads all in flight together: one L2/HBM round trip
         constexpr int KB = (int)sizeof(KT);
-        const int n16 = np * hd * KB / 16;
         const int vpr = hd * KB / 16;  // 16-byte vectors per K/V row
-        const uint4* gk = reinterpret_cast<const uint4*>(reinterpret_cast<const KT*>(a.k_cache) + kvbase + (int64_t)p0 * hd);
-        const uint4* gv = reinterpret_cast<const uint4*>(reinterpret_cast<const KT*>(a.v_cache) + kvbase + (int64_t)p0 * hd);
-        for (int o = tid; o < G * hd; o += NT) s.u.a.q[o] = __ldcg(a.q + (int64_t)g * G * hd + o);
-#pragma unroll 1
-        {  // n16 <= ATT_STAGE / 16 = 4 * NT: every thread's loads in flight together
-            constexpr int PER = ATT_STAGE / 16 / NT;
-            uint4 kk[PER], vv[PER];
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const int v = tid + q * NT;
-                if (v < n16) { kk[q] = __ldcg(gk + v); vv[q] = __ldcg(gv + v); }
-            }
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const int v = tid + q * NT;
-                if (v < n16) {
-                    s.u.a.k[(v / vpr) * (vpr + 4) + v % vpr] = kk[q];  // K row p at p*(vpr+4) (64-B pad)
-                    s.u.a.v[v] = vv[q];
-                }
-            }
-        }
+        // the step's new position: with the qkv accumulator its row is built
+        // from the accumulator (not read from the cache)
+        const int pos = L - 1;
+        const int newrow = (a.qkv_acc && pos >= p0 && pos < p1) ? pos - p0 : -1;
+        attn_stage<KT>(a, g, p0, np, pos, newrow, kvbase, s);
         __syncthreads();
         ATT_STAMP(2);
         const KT* vs = reinterpret_cast<const KT*>(s.u.a.v);
@@ -1013,8 +1091,8 @@ __device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, S
     for (int u = (int)(((int64_t)cr * nu + G - 1) / G); u < nu && (int64_t)u * G / nu == cr; ++u) {
         const int g = u % a.KVH, ch = u / a.KVH;
         wait_range(P.counters, a.dep_base + g, a.dep_base + g, a.dep_target[g]);
-        if (a.kv_dtype == TEAL_BF16) attn_unit_t<uint16_t>(P, a, g, ch, s);
-        else attn_unit_t<float>(P, a, g, ch, s);
+        if (a.kv_dtype == TEAL_BF16) attn_unit_t<uint16_t>(P, a, g, ch, L, s);
+        else attn_unit_t<float>(P, a, g, ch, L, s);
         __syncthreads();
     }
 }

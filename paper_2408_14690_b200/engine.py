@@ -56,7 +56,7 @@ class StepAttn(ctypes.Structure):
     _fields_ = [("q", c_vp), ("k_cache", c_vp), ("v_cache", c_vp), ("ctx", c_vp), ("partials", c_vp),
                 ("tickets", c_vp), ("max_seq", c_i64), ("H", c_i), ("KVH", c_i), ("hd", c_i), ("kv_dtype", c_i),
                 ("chunk", c_i), ("nchunks", c_i), ("sig_base", c_i), ("dep_base", c_i), ("dep_target", c_vp),
-                ("dbg", c_vp)]
+                ("dbg", c_vp), ("qkv_acc", c_vp), ("rope_cos", c_vp), ("rope_sin", c_vp), ("nq", c_i), ("nkv", c_i)]
 
 
 class StepPhase(ctypes.Structure):
@@ -74,6 +74,8 @@ class StepPlan(ctypes.Structure):
 
 PHASE_LOAD, PHASE_GEMV, PHASE_ATTN, PHASE_RESID = 0, 1, 2, 3
 PRO_RMS_ACC, PRO_SILU_ACC = 2, 3
+import os as _os
+_NO_QKV_ACC = _os.environ.get("TEAL_NO_QKV_ACC") == "1"
 CONTRIB = 1024  # TEAL_STEP_CONTRIB: counter units per finished tile of an ACC output
 XS_MAX = 8192   # PRO_RMS_ACC staging limit on d
 DEP_NONE, DEP_GLOBAL, DEP_ROWS = 0, 1, 2
@@ -407,13 +409,14 @@ class StepDecoder:
         rec = G * hd + 2 * G
         self.ws["attn"] = torch.zeros(KVH * self.nchunks * rec, device=dev)
         # ACC accumulators per layer (int64 fixed point, zeroed by every step's
-        # load phase): o and down deltas of the residual [d], gate/up [nt_gu*TW]
-        per_acc = 2 * d + nt_gu * TW
+        # load phase): o and down deltas of the residual [d], gate/up [nt_gu*TW],
+        # q|k|v [nt_qkv*TW]
+        per_acc = 2 * d + nt_gu * TW + nt_qkv * TW
         self.acc = torch.zeros(L * per_acc, device=dev, dtype=torch.int64)
 
         def accs(l):
             b = self.acc[l * per_acc:(l + 1) * per_acc]
-            return dict(o=b[:d], down=b[d:2 * d], gu=b[2 * d:])
+            return dict(o=b[:d], down=b[d:2 * d], gu=b[2 * d:2 * d + nt_gu * TW], qkv=b[2 * d + nt_gu * TW:])
         K_ = CONTRIB
 
         groups, attns, phases, keep = [], [], [], []
@@ -456,19 +459,20 @@ class StepDecoder:
                 tv = _t32(t[seg])
                 meta.append(StepTile(tv, tv, seg, seg, int(first), int(first), cb["attn"] + g0, cb["attn"] + g1))
             groups.append(self._group(tw["qkv"], tiles_tensor(meta), m=d, n=nq + 2 * nkv, maxc=mc["qkv"],
-                                      gain=lw.rms_attn, ws="qkv", **qkv_in,
+                                      gain=lw.rms_attn, ws="qkv", **qkv_in, acc=None if _NO_QKV_ACC else A["qkv"],
                                       epilogue=SEPI_QKV, q_out=self.q, k_cache=kc, v_cache=vc,
                                       dbg=(T.h["pre_attn"][l] if T else None,
                                            [T.bits[p][l] for p in ("q", "k", "v")] if T else None,
                                            [K[l, PROJ.index(p)] for p in ("q", "k", "v")] if K is not None else None)))
             phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_GLOBAL, dep_in[0], dep_in[1], 1))
             # --- attention per (kv group, position chunk)
-            tgt = torch.tensor(feeds, dtype=torch.int32, device=dev)
+            tgt = torch.tensor([f_ * (1 if _NO_QKV_ACC else K_) for f_ in feeds], dtype=torch.int32, device=dev)
             keep.append(tgt)
             attns.append(StepAttn(self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(), self.ctx.data_ptr(),
                                   self.ws["attn"].data_ptr(), self.tk["attn"].data_ptr(), spec.max_seq,
                                   spec.n_heads, KVH, hd, RT.dtype_code(self.kv_dtype), self.attn_chunk,
-                                  self.nchunks, cb["odep"], cb["attn"], tgt.data_ptr(), RT.ptr(self.attn_dbg)))
+                                  self.nchunks, cb["odep"], cb["attn"], tgt.data_ptr(), RT.ptr(self.attn_dbg),
+                                  None if _NO_QKV_ACC else A["qkv"].data_ptr(), RT.ptr(self.rope_cos), RT.ptr(self.rope_sin), nq, nkv))
             phases.append(StepPhase(PHASE_ATTN, len(attns) - 1, DEP_NONE, 0, 0, 1))
             # --- o: rows = context channels, each waits for its kv group's context
             tv = _t32(t[3])
