@@ -53,7 +53,7 @@ constexpr int ATT_MAXG = 8;
 constexpr int ATT_MAXHD = 128;
 constexpr int ATT_MAXCHUNK = 256;
 constexpr int ATT_STAGE = 16384;  // bytes of K (and of V) staged per attention unit
-constexpr int ATT_MAXCHUNK_STAGE = 128;  // staged positions (>= 16384 / (hd * kv bytes))
+                                  // (engine: chunk <= 16384 / (hd * kv bytes))
 constexpr int XS_MAX = 8192;      // PRO_RMS_ACC: the CTA's copy of x' (m <= XS_MAX)
 constexpr int CONTRIB = TEAL_STEP_CONTRIB;
 static_assert(NT == TW, "epilogues map one thread per tile column");
@@ -69,8 +69,8 @@ struct Smem {
         struct {
             float q[ATT_MAXG * ATT_MAXHD];
             float sc[ATT_MAXG * ATT_MAXCHUNK];
-            uint4 k[ATT_STAGE / 16 + 4 * ATT_MAXCHUNK_STAGE];  // K rows, each padded by 64 B (bank-conflict free)
-            uint4 v[ATT_STAGE / 16];   // V rows of the chunk
+            uint4 k[ATT_STAGE / 16 + ATT_MAXCHUNK];  // K rows (cache dtype), each padded by 16 B
+            uint4 v[ATT_STAGE / 16];                 // V rows of the chunk
         } a;
     } u;
     float red[NW * TW];
@@ -794,23 +794,51 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
 // One kernel instantiation per weight format: every GEMV group of a plan
 // (layers and LM head) uses the plan's w_dtype.
 
-// Stage one attention unit's inputs in shared memory: q of kv group g
-// (from the plan's q vector, or from the qkv accumulator with RoPE applied)
-// and the chunk's np K / V rows from the cache.  With the accumulator, the
-// row of the step's new position (newrow >= 0) is built from it instead: k
-// (RoPE) and v, also written to the cache.  Every load of the thread is in
-// flight before any is consumed (one L2 round trip).
-template <typename KT>
-__device__ __noinline__ void attn_stage(const teal_step_attn& a, int g, int p0, int np, int pos, int newrow,
-                                        int64_t kvbase, Smem& s) {
-    constexpr int KB = (int)sizeof(KT);
-    constexpr int QPT = ATT_MAXG * ATT_MAXHD / NT;
+// ---- attention unit: (kv group g, position chunk) ---------------------------
+// Runs on a few CTAs once per layer, so its instructions are cold every time
+// (the kernel is far larger than the 32 KB L1.5 instruction cache): the code
+// is deliberately small — runtime loops, no unrolling over heads, the K/V
+// dtype a runtime switch around two short inner loops — since instruction
+// fetch from L2, not arithmetic, sets its latency.
+//
+// Staging in two parts.  attn_stage_kv runs BEFORE the unit's q/k/v tiles are
+// done (the cache rows of earlier positions do not depend on this step): the
+// chunk's np K / V rows except the new position's (newrow) -> smem (cache
+// dtype; K rows padded by 16 B so row-parallel reads are conflict-free).
+// attn_stage_q runs after the wait: q of group g (RoPE applied when it comes
+// from the accumulator) and the new row's k (RoPE) and v, which it also
+// appends to the cache (rounded to the cache dtype first, as later steps will
+// read it).
+
+__device__ __noinline__ void attn_stage_kv(const teal_step_attn& a, int p0, int np, int newrow, int64_t kvbase,
+                                           Smem& s) {
     constexpr int PER = ATT_STAGE / 16 / NT;  // n16 <= ATT_STAGE / 16 = PER * NT
+    const int tid = threadIdx.x, hd = a.hd;
+    const int kvb = a.kv_dtype == TEAL_BF16 ? 2 : 4;
+    const int vpr = hd * kvb / 16;  // 16-byte vectors per row
+    const int n16 = np * vpr;
+    const uint4* gk = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(a.k_cache) + (kvbase + (int64_t)p0 * hd) * kvb);
+    const uint4* gv = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(a.v_cache) + (kvbase + (int64_t)p0 * hd) * kvb);
+    uint4 kk[PER], vv[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int v = tid + q * NT;
+        if (v < n16 && v / vpr != newrow) { kk[q] = __ldcg(gk + v); vv[q] = __ldcg(gv + v); }
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int v = tid + q * NT;
+        if (v < n16 && v / vpr != newrow) {
+            s.u.a.k[(v / vpr) * (vpr + 1) + v % vpr] = kk[q];
+            s.u.a.v[v] = vv[q];
+        }
+    }
+}
+
+__device__ __noinline__ void attn_stage_q(const teal_step_attn& a, int g, int pos, int newrow, int64_t kvbase,
+                                          Smem& s) {
+    constexpr int QPT = ATT_MAXG * ATT_MAXHD / NT;
     const int tid = threadIdx.x, G = a.H / a.KVH, hd = a.hd, half = hd >> 1;
-    const int n16 = np * hd * KB / 16;
-    const int vpr = hd * KB / 16;  // 16-byte vectors per K/V row
-    const uint4* gk = reinterpret_cast<const uint4*>(reinterpret_cast<const KT*>(a.k_cache) + kvbase + (int64_t)p0 * hd);
-    const uint4* gv = reinterpret_cast<const uint4*>(reinterpret_cast<const KT*>(a.v_cache) + kvbase + (int64_t)p0 * hd);
     const bool acc = a.qkv_acc != nullptr;
     // NT is a multiple of hd: every element this thread touches (q heads and
     // the new k) has head dim d = tid % hd, so one RoPE pair serves all
@@ -846,12 +874,6 @@ __device__ __noinline__ void attn_stage(const teal_step_attn& a, int g, int p0, 
         if (rope) kp = __ldcg(a.qkv_acc + kc + part);
         va = __ldcg(a.qkv_acc + kc + a.nkv);
     }
-    uint4 kk[PER], vv[PER];
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int v = tid + q * NT;
-        if (v < n16 && v / vpr != newrow) { kk[q] = __ldcg(gk + v); vv[q] = __ldcg(gv + v); }
-    }
     const float sgn = d < half ? -1.f : 1.f;  // x*cos -/+ partner*sin
 #pragma unroll
     for (int j = 0; j < QPT; ++j) {
@@ -863,42 +885,30 @@ __device__ __noinline__ void attn_stage(const teal_step_attn& a, int g, int p0, 
         }
     }
     if (nk) {
-        const float kr = rope ? fmaf(sgn * from_fx(kp), sn, from_fx(ka) * cs) : from_fx(ka);
-        const float vr = from_fx(va);
+        float kr = rope ? fmaf(sgn * from_fx(kp), sn, from_fx(ka) * cs) : from_fx(ka);
+        float vr = from_fx(va);
         const int64_t off = kvbase + (int64_t)pos * hd + d;
-        KT* kst = reinterpret_cast<KT*>(s.u.a.k) + (int64_t)newrow * (vpr + 4) * (16 / KB) + d;
-        KT* vst = reinterpret_cast<KT*>(s.u.a.v) + (int64_t)newrow * hd + d;
-        if constexpr (KB == 2) {
+        if (a.kv_dtype == TEAL_BF16) {
             const uint16_t kb = f32_to_bf16_rn(kr), vb = f32_to_bf16_rn(vr);
             reinterpret_cast<uint16_t*>(const_cast<void*>(a.k_cache))[off] = kb;
             reinterpret_cast<uint16_t*>(const_cast<void*>(a.v_cache))[off] = vb;
-            *kst = kb;
-            *vst = vb;
         } else {
             reinterpret_cast<float*>(const_cast<void*>(a.k_cache))[off] = kr;
             reinterpret_cast<float*>(const_cast<void*>(a.v_cache))[off] = vr;
-            *kst = kr;
-            *vst = vr;
         }
-    }
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int v = tid + q * NT;
-        if (v < n16 && v / vpr != newrow) {
-            s.u.a.k[(v / vpr) * (vpr + 4) + v % vpr] = kk[q];  // K row p at p*(vpr+4) (64-B pad)
-            s.u.a.v[v] = vv[q];
+        const int vpr = hd * (a.kv_dtype == TEAL_BF16 ? 2 : 4) / 16;
+        if (a.kv_dtype == TEAL_BF16) {
+            reinterpret_cast<uint16_t*>(s.u.a.k + newrow * (vpr + 1))[d] = f32_to_bf16_rn(kr);
+            reinterpret_cast<uint16_t*>(s.u.a.v)[newrow * hd + d] = f32_to_bf16_rn(vr);
+        } else {
+            reinterpret_cast<float*>(s.u.a.k + newrow * (vpr + 1))[d] = kr;
+            reinterpret_cast<float*>(s.u.a.v)[newrow * hd + d] = vr;
         }
     }
 }
 
-// ---- attention unit: (kv head g, position chunk) -------------------------------
-// Deliberately compact code (runtime loops over heads and head_dim chunks):
-// this path runs on a few CTAs once per layer, so its instructions are cold
-// in the instruction cache every time; unrolled code here costs more in
-// instruction fetch than it saves in issue slots.
-template <typename KT>
-__device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_step_attn& a, int g, int ch, int L,
-                                        Smem& s) {
+__device__ __noinline__ void attn_unit(const teal_step_plan& P, const teal_step_attn& a, int g, int ch, int L,
+                                       Smem& s) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = a.H / a.KVH, hd = a.hd;
     const int p0 = ch * a.chunk;
@@ -910,73 +920,50 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
     unsigned long long* dbg = a.dbg ? a.dbg + ((int64_t)g * a.nchunks + ch) * 6 : nullptr;
 #define ATT_STAMP(k) do { if (dbg && tid == 0) dbg[k] = gtimer(); } while (0)
     ATT_STAMP(0);
+    const int pos = L - 1;
+    const int newrow = (a.qkv_acc && pos >= p0 && pos < p1) ? pos - p0 : -1;
+    if (np > 0) attn_stage_kv(a, p0, np, newrow, kvbase, s);
+    wait_range(P.counters, a.dep_base + g, a.dep_base + g, a.dep_target[g]);  // q / new row ready
     if (np > 0) {
-        constexpr int KB = (int)sizeof(KT);
-        const int vpr = hd * KB / 16;  // 16-byte vectors per K/V row
-        // the step's new position: with the qkv accumulator its row is built
-        // from the accumulator (not read from the cache)
-        const int pos = L - 1;
-        const int newrow = (a.qkv_acc && pos >= p0 && pos < p1) ? pos - p0 : -1;
-        attn_stage<KT>(a, g, p0, np, pos, newrow, kvbase, s);
+        attn_stage_q(a, g, pos, newrow, kvbase, s);
         __syncthreads();
         ATT_STAMP(2);
-        const KT* vs = reinterpret_cast<const KT*>(s.u.a.v);
-        const float den = sqrtf((float)hd);
-        // scores: 4 threads per position; thread dq takes the row's 16-byte
-        // chunks dq, dq+4, ... (K rows padded by 64 B and the interleaved
-        // chunks make both the K and the q reads bank-conflict free); the K
-        // chunk is loaded once and used for every head; 2 shuffles combine.
-        {
-            const int dq = tid & 3, pl = tid >> 2;
-            constexpr int EPC = 16 / KB;  // elements per 16-byte chunk
+        // scores: thread -> (head, position) pairs, 4 independent chains
+        const float rs = rsqrtf((float)hd);
+        const bool bf = a.kv_dtype == TEAL_BF16;
+        const int vpr = hd * (bf ? 2 : 4) / 16;
 #pragma unroll 1
-            for (int p = pl; p < (np + 63) / 64 * 64; p += NT / 4) {
-                const bool pv = p < np;
-                const uint4* kr = s.u.a.k + (pv ? p : 0) * (vpr + 4);
-                float dot[ATT_MAXG];
-#pragma unroll
-                for (int h = 0; h < ATT_MAXG; ++h) dot[h] = 0.f;
-#pragma unroll 1
-                for (int c = dq; c < vpr; c += 4) {
-                    const uint4 raw = kr[c];
-                    float kv[8];
-                    if constexpr (KB == 2) {
-                        const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) { kv[2 * k] = bf16_lo(u[k]); kv[2 * k + 1] = bf16_hi(u[k]); }
-                    } else {
-                        kv[0] = __uint_as_float(raw.x); kv[1] = __uint_as_float(raw.y);
-                        kv[2] = __uint_as_float(raw.z); kv[3] = __uint_as_float(raw.w);
-                    }
-#pragma unroll
-                    for (int h = 0; h < ATT_MAXG; ++h) {
-                        if (h < G) {
-                            const float4* qv = reinterpret_cast<const float4*>(s.u.a.q + h * hd + c * EPC);
-                            const float4 q0 = qv[0];
-                            dot[h] = fmaf(q0.x, kv[0], dot[h]);
-                            dot[h] = fmaf(q0.y, kv[1], dot[h]);
-                            dot[h] = fmaf(q0.z, kv[2], dot[h]);
-                            dot[h] = fmaf(q0.w, kv[3], dot[h]);
-                            if constexpr (EPC == 8) {
-                                const float4 q1 = qv[1];
-                                dot[h] = fmaf(q1.x, kv[4], dot[h]);
-                                dot[h] = fmaf(q1.y, kv[5], dot[h]);
-                                dot[h] = fmaf(q1.z, kv[6], dot[h]);
-                                dot[h] = fmaf(q1.w, kv[7], dot[h]);
-                            }
-                        }
-                    }
+        for (int i = tid; i < G * np; i += NT) {
+            const int h = i / np, p = i - h * np;
+            const float4* qv = reinterpret_cast<const float4*>(s.u.a.q + h * hd);
+            const uint4* kv = s.u.a.k + p * (vpr + 1);
+            float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (bf) {
+#pragma unroll 2
+                for (int c = 0; c < vpr; ++c) {  // 8 elements per 16 B
+                    const uint4 y = kv[c];
+                    const float4 x0 = qv[2 * c], x1 = qv[2 * c + 1];
+                    acc4.x = fmaf(x0.x, bf16_lo(y.x), acc4.x);
+                    acc4.y = fmaf(x0.y, bf16_hi(y.x), acc4.y);
+                    acc4.z = fmaf(x0.z, bf16_lo(y.y), acc4.z);
+                    acc4.w = fmaf(x0.w, bf16_hi(y.y), acc4.w);
+                    acc4.x = fmaf(x1.x, bf16_lo(y.z), acc4.x);
+                    acc4.y = fmaf(x1.y, bf16_hi(y.z), acc4.y);
+                    acc4.z = fmaf(x1.z, bf16_lo(y.w), acc4.z);
+                    acc4.w = fmaf(x1.w, bf16_hi(y.w), acc4.w);
                 }
-#pragma unroll
-                for (int h = 0; h < ATT_MAXG; ++h) {
-                    if (h < G) {
-                        float d = dot[h];
-                        d += __shfl_xor_sync(0xffffffffu, d, 1);
-                        d += __shfl_xor_sync(0xffffffffu, d, 2);
-                        if (pv && dq == 0) s.u.a.sc[h * ATT_MAXCHUNK + p] = d / den;
-                    }
+            } else {
+#pragma unroll 2
+                for (int c = 0; c < vpr; ++c) {
+                    const uint4 y = kv[c];
+                    const float4 x = qv[c];
+                    acc4.x = fmaf(x.x, __uint_as_float(y.x), acc4.x);
+                    acc4.y = fmaf(x.y, __uint_as_float(y.y), acc4.y);
+                    acc4.z = fmaf(x.z, __uint_as_float(y.z), acc4.z);
+                    acc4.w = fmaf(x.w, __uint_as_float(y.w), acc4.w);
                 }
             }
+            s.u.a.sc[h * ATT_MAXCHUNK + p] = ((acc4.x + acc4.y) + (acc4.z + acc4.w)) * rs;
         }
         __syncthreads();
         ATT_STAMP(1);
@@ -996,24 +983,35 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
             if (lane == 0) { s.am[h] = mx; s.al[h] = l; }
         }
         __syncthreads();
-        // context partial: thread -> (head, d), positions ascending.  A
-        // single chunk holding every position is final: normalise and write
-        // the context directly (no partial record, ticket or combine).
+        // context partial: thread -> (head, d), positions ascending in two
+        // chains (even / odd).  A single chunk holding every position is
+        // final: normalise and write the context (no record, ticket, combine).
         const bool single = (p0 == 0 && p1 == L);
 #pragma unroll 1
         for (int o = tid; o < G * hd; o += NT) {
-            const int h = o / hd, d = o - h * hd;
+            const int h = o / hd, dd = o - h * hd;
             const float* pr = s.u.a.sc + h * ATT_MAXCHUNK;
-            float acc0 = 0.f, acc1 = 0.f;  // two chains (even / odd positions), summed at the end
+            float c0 = 0.f, c1 = 0.f;
+            if (bf) {
+                const uint16_t* vc = reinterpret_cast<const uint16_t*>(s.u.a.v) + dd;
 #pragma unroll 4
-            for (int p = 0; p + 1 < np; p += 2) {
-                acc0 = fmaf(pr[p], to_f32<KT>(vs[p * hd + d]), acc0);
-                acc1 = fmaf(pr[p + 1], to_f32<KT>(vs[(p + 1) * hd + d]), acc1);
+                for (int p = 0; p + 1 < np; p += 2) {
+                    c0 = fmaf(pr[p], bf16_to_f32(vc[p * hd]), c0);
+                    c1 = fmaf(pr[p + 1], bf16_to_f32(vc[(p + 1) * hd]), c1);
+                }
+                if (np & 1) c0 = fmaf(pr[np - 1], bf16_to_f32(vc[(np - 1) * hd]), c0);
+            } else {
+                const float* vc = reinterpret_cast<const float*>(s.u.a.v) + dd;
+#pragma unroll 4
+                for (int p = 0; p + 1 < np; p += 2) {
+                    c0 = fmaf(pr[p], vc[p * hd], c0);
+                    c1 = fmaf(pr[p + 1], vc[(p + 1) * hd], c1);
+                }
+                if (np & 1) c0 = fmaf(pr[np - 1], vc[(np - 1) * hd], c0);
             }
-            if (np & 1) acc0 = fmaf(pr[np - 1], to_f32<KT>(vs[(np - 1) * hd + d]), acc0);
-            const float acc = acc0 + acc1;
-            if (single) a.ctx[(int64_t)g * G * hd + o] = acc / s.al[h];
-            else __stcg(my + o, acc);
+            const float r = c0 + c1;
+            if (single) a.ctx[(int64_t)g * G * hd + o] = r / s.al[h];
+            else __stcg(my + o, r);
         }
         if (single) {
             ATT_STAMP(3);
@@ -1032,12 +1030,11 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
     }
     ATT_STAMP(2);
     // only the chunks holding positions take part (the attn phase skips the rest)
-    const int nact_t = min(a.nchunks, (L + a.chunk - 1) / a.chunk);
-    const bool last = take_ticket(a.tickets + g, (unsigned)nact_t - 1u, s.last);
+    const int nact = min(a.nchunks, (L + a.chunk - 1) / a.chunk);
+    const bool last = take_ticket(a.tickets + g, (unsigned)nact - 1u, s.last);
     ATT_STAMP(3);
     if (!last) return;
     const float* rb = a.partials + (int64_t)g * a.nchunks * rec;
-    const int nact = min(a.nchunks, (L + a.chunk - 1) / a.chunk);  // chunks holding positions
     for (int q = tid; q < nact * 2 * G; q += NT) {  // (m, l) of every active chunk -> smem
         const int c = q / (2 * G), k = q % (2 * G);
         s.u.a.sc[q] = __ldcg(rb + (int64_t)c * rec + G * hd + k);
@@ -1049,13 +1046,13 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
         float M = -INFINITY;
         for (int c = 0; c < nact; ++c)
             if (s.u.a.sc[c * 2 * G + G + h] > 0.f) M = fmaxf(M, s.u.a.sc[c * 2 * G + h]);
-        float num = 0.f, dd = 0.f;
+        float num = 0.f, dn = 0.f;
 #pragma unroll 1
         for (int c0 = 0; c0 < nact; c0 += 4) {
             float pv[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) pv[q] = (c0 + q < nact) ? __ldcg(rb + (int64_t)(c0 + q) * rec + o) : 0.f;
-#pragma unroll
+#pragma unroll 1
             for (int q = 0; q < 4; ++q) {
                 const int c = c0 + q;
                 if (c < nact) {
@@ -1063,12 +1060,12 @@ __device__ __noinline__ void attn_unit_t(const teal_step_plan& P, const teal_ste
                     if (ls > 0.f) {
                         const float sc = expf(s.u.a.sc[c * 2 * G + h] - M);
                         num = fmaf(pv[q], sc, num);
-                        dd = fmaf(ls, sc, dd);
+                        dn = fmaf(ls, sc, dn);
                     }
                 }
             }
         }
-        a.ctx[(int64_t)g * G * hd + o] = num / dd;
+        a.ctx[(int64_t)g * G * hd + o] = num / dn;
     }
     ATT_STAMP(4);
     signal(P.counters, a.sig_base + g, a.sig_base + g);
@@ -1089,10 +1086,8 @@ __device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, S
     // spread over the grid from its end (the qkv phase leaves the last CTAs idle)
     const int cr = G - 1 - (int)blockIdx.x;
     for (int u = (int)(((int64_t)cr * nu + G - 1) / G); u < nu && (int64_t)u * G / nu == cr; ++u) {
-        const int g = u % a.KVH, ch = u / a.KVH;
-        wait_range(P.counters, a.dep_base + g, a.dep_base + g, a.dep_target[g]);
-        if (a.kv_dtype == TEAL_BF16) attn_unit_t<uint16_t>(P, a, g, ch, L, s);
-        else attn_unit_t<float>(P, a, g, ch, L, s);
+        const int g = u % a.KVH, ch = u / a.KVH;  // (the unit waits for its q/k/v tiles itself)
+        attn_unit(P, a, g, ch, L, s);
         __syncthreads();
     }
 }
