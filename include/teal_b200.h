@@ -315,6 +315,10 @@ typedef struct teal_step_group {
     long long* acc;          /* nullable ACC output [ntiles*TW] (zero at step start) */
     const long long* in_acc; /* PRO_RMS_ACC: delta [m]; PRO_SILU_ACC: gate/up accumulator */
     float* x_out;            /* PRO_RMS_ACC / PHASE_RESID: materialised x' [m]  */
+    const int4* ranges;      /* nullable ACC work split: CTA c < nranges takes 32-row
+                                groups [x, y) (at most two tiles) and bumps its first /
+                                second tile's counters by z / w; NULL: equal split */
+    int nranges, pad2_;
 } teal_step_group;
 
 typedef struct teal_step_attn {

@@ -677,9 +677,13 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gpt = (g.m + 31) / 32;
     const int64_t F = (int64_t)g.ntiles * gpt;
-    const int G = participants(g.ntiles, F), c = blockIdx.x;
+    const int c = blockIdx.x;
+    const int G = g.ranges ? g.nranges : participants(g.ntiles, F);
     if (c >= G) return;
-    const int64_t g0 = (int64_t)c * F / G, g1 = (int64_t)(c + 1) * F / G;
+    int4 rg = make_int4(0, 0, 0, 0);
+    if (g.ranges) rg = g.ranges[c];
+    const int64_t g0 = g.ranges ? (int64_t)rg.x : (int64_t)c * F / G;
+    const int64_t g1 = g.ranges ? (int64_t)rg.y : (int64_t)(c + 1) * F / G;
     const bool rms = g.prologue == TEAL_PRO_RMSNORM || g.prologue == TEAL_PRO_RMS_ACC;
     // While this slice waits for its inputs, pull the head of its weight range
     // into L2 (one bulk prefetch of contiguous tiled rows): the wait is tail
@@ -751,7 +755,8 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
         if (g.acc) {  // ACC output: add this CTA's partial, bump the counters by its share of CONTRIB
             if (g.col_scale) v *= g.col_scale[(int64_t)tile * TW + tid];
             red_add_s64(g.acc + (int64_t)tile * TW + tid, to_fx(v));
-            signal(P.counters, tm.sig0, tm.sig1, c == cf ? CONTRIB - (cl - cf) : 1);
+            signal(P.counters, tm.sig0, tm.sig1,
+                   g.ranges ? (segi == 0 ? rg.z : rg.w) : (c == cf ? CONTRIB - (cl - cf) : 1));
             ++lasts;
             if (segi == 0) SL_STAMP(4, gtimer());
             continue;

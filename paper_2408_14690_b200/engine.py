@@ -49,7 +49,7 @@ class StepGroup(ctypes.Structure):
                 ("prologue", c_i), ("nss", c_i), ("eps", c_f), ("epilogue", c_i),
                 ("nq", c_i), ("nkv", c_i), ("head_dim", c_i), ("kv_dtype", c_i), ("w_dtype", c_i),
                 ("gscale", c_vp), ("group", c_i), ("t_all", c_f), ("tile_stride_b", c_i64), ("row_stride_b", c_i64),
-                ("acc", c_vp), ("in_acc", c_vp), ("x_out", c_vp)]
+                ("acc", c_vp), ("in_acc", c_vp), ("x_out", c_vp), ("ranges", c_vp), ("nranges", c_i), ("pad2_", c_i)]
 
 
 class StepAttn(ctypes.Structure):
@@ -101,6 +101,59 @@ def max_contributors(ntiles: int, m: int, G: int) -> int:
     def owner(x):
         return ((x + 1) * G - 1) // F
     return max(owner((t + 1) * gpt - 1) - owner(t * gpt) + 1 for t in range(ntiles))
+
+
+def weighted_ranges(ntiles: int, m: int, grid: int, penalty: int):
+    """Work split of an ACC group whose equal ranges would cross tiles: CTA
+    ranges of 32-row groups where a range spanning two tiles is charged
+    `penalty` extra groups (its second compaction / reduction / ramp-up), so
+    the two-tile CTAs, which gate half the tiles, finish with the rest.
+    Returns [(g0, g1, w_first_tile, w_second_tile)] per CTA (counter weights:
+    the first contributor of a tile adds CONTRIB - (contributors - 1), the
+    others 1), or None when the equal split already keeps ranges in one tile."""
+    gpt = -(-m // 32)
+    F = ntiles * gpt
+    if participants(ntiles, F, grid) != grid or F <= grid or penalty <= 0 or F > grid * gpt:
+        return None
+    if grid % ntiles == 0 or all((c * F // grid) // gpt == ((c + 1) * F // grid - 1) // gpt for c in range(grid)):
+        return None
+
+    def split(T):
+        out, g = [], 0
+        while g < F:
+            t = g // gpt
+            end1 = (t + 1) * gpt
+            if end1 - g >= T:           # fits in this tile
+                e = g + T
+            elif end1 - g + penalty < T and end1 < F:  # spill into the next tile (never a third)
+                e = min(F, end1 + gpt - 1, g + T - penalty)
+            else:
+                e = end1
+            out.append((g, e))
+            g = e
+        return out
+
+    lo, hi = 1, F
+    while lo < hi:
+        T = (lo + hi) // 2
+        if len(split(T)) <= grid:
+            hi = T
+        else:
+            lo = T + 1
+    rs = split(lo)
+    contrib = {}
+    for i, (a, b) in enumerate(rs):
+        for t in range(a // gpt, (b - 1) // gpt + 1):
+            contrib.setdefault(t, []).append(i)
+    res = []
+    for i, (a, b) in enumerate(rs):
+        ws = []
+        for t in range(a // gpt, (b - 1) // gpt + 1):
+            cs = contrib[t]
+            ws.append(CONTRIB - (len(cs) - 1) if cs[0] == i else 1)
+        ws += [0] * (2 - len(ws))
+        res.append((a, b, ws[0], ws[1]))
+    return res
 
 
 _BOUND = False
@@ -524,6 +577,20 @@ class StepDecoder:
             self.cand_v = torch.zeros(1, device=dev)
             self.cand_i = torch.zeros(1, device=dev, dtype=torch.int32)
         self.lm_done = torch.zeros(1, device=dev, dtype=torch.int32)
+        # ACC groups whose equal split crosses tiles (gate/up): weighted ranges
+        import os
+        pen = int(os.environ.get("TEAL_SEG_PENALTY", "10"))  # measured: 0 -> 31.7 us, 10 -> 29.5 us gate/up
+        self.range_tables = {}
+        for gi, g in enumerate(groups):
+            if not g.acc or g.m <= 0:
+                continue
+            key = (g.ntiles, g.m)
+            if key not in self.range_tables:
+                rs = weighted_ranges(g.ntiles, g.m, Gc, pen)
+                self.range_tables[key] = None if rs is None else torch.tensor(rs, dtype=torch.int32, device=dev)
+            tab = self.range_tables[key]
+            if tab is not None:
+                g.ranges, g.nranges = tab.data_ptr(), tab.shape[0]
         self._keep = keep
         self._groups = dev_bytes((StepGroup * len(groups))(*groups))
         self._attns = dev_bytes((StepAttn * len(attns))(*attns))
