@@ -318,7 +318,13 @@ typedef struct teal_step_group {
     const int4* ranges;      /* nullable ACC work split: CTA c < nranges takes 32-row
                                 groups [x, y) (at most two tiles) and bumps its first /
                                 second tile's counters by z / w; NULL: equal split */
-    int nranges, pad2_;
+    int nranges;
+    int xsig;                /* PRO_RMS_ACC: counter bumped by each CTA once its x_out share is
+                                written (-1: none)                                      */
+    int xwait, xwait_target; /* PRO_RMS_ACC: x (the previous version) is complete when
+                                counters[xwait] >= xwait_target; it is then staged before
+                                the phase's own dependency wait (-1: stage after it)   */
+    int pad3_;
 } teal_step_group;
 
 typedef struct teal_step_attn {

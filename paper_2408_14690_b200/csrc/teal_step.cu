@@ -401,34 +401,48 @@ __device__ __forceinline__ float rms_den(const teal_step_group& g, int lane) {
     return sqrtf(a / (float)g.m + g.eps);
 }
 
-// PRO_RMS_ACC: x' = x + fx(in_acc) over all m channels into s.u.g.xs (every
-// load in flight at once), CTA c of G writes its share [c*m/G, (c+1)*m/G) of
-// x' to x_out (the next residual version), and returns the RMSNorm
-// denominator.  Every CTA computes the same sum in the same order, so all
-// tiles threshold the same h.
-__device__ float rms_acc_prep(const teal_step_group& g, int c, int G, Smem& s) {
+// PRO_RMS_ACC, in two parts.  rms_stage_x: the previous residual version x
+// (final since an earlier phase) -> s.u.g.xs, issued while the phase still
+// waits for its accumulator.  rms_acc_finish: x' = x + fx(in_acc) over all m
+// channels (every load in flight at once), CTA c of G writes its share
+// [c*m/G, (c+1)*m/G) of x' to x_out (the next residual version), and the
+// RMSNorm denominator is returned.  Every CTA computes the same sum in the
+// same order, so all tiles threshold the same h.
+__device__ void rms_stage_x(const teal_step_group& g, Smem& s) {
+    const int tid = threadIdx.x, m = g.m;
+#pragma unroll 1
+    for (int i0 = 0; i0 < m; i0 += 16 * NT) {
+        float xb[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int i = i0 + q * NT + tid;
+            xb[q] = i < m ? __ldcg(g.x + i) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int i = i0 + q * NT + tid;
+            if (i < m) s.u.g.xs[i] = xb[q];
+        }
+    }
+}
+
+__device__ float rms_acc_finish(const teal_step_group& g, int c, int G, Smem& s) {
     const int tid = threadIdx.x, m = g.m;
     const int p0 = (int)((int64_t)c * m / G), p1 = (int)((int64_t)(c + 1) * m / G);
     float ss = 0.f;
 #pragma unroll 1
     for (int i0 = 0; i0 < m; i0 += 16 * NT) {
-        float xb[16];
         long long xa[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
             const int i = i0 + q * NT + tid;
-            xb[q] = 0.f;
-            xa[q] = 0;
-            if (i < m) {
-                xb[q] = __ldcg(g.x + i);
-                xa[q] = __ldcg(g.in_acc + i);
-            }
+            xa[q] = i < m ? __ldcg(g.in_acc + i) : 0;
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
             const int i = i0 + q * NT + tid;
             if (i < m) {
-                const float xn = xb[q] + from_fx(xa[q]);
+                const float xn = s.u.g.xs[i] + from_fx(xa[q]);  // own thread's staged x: no barrier needed
                 s.u.g.xs[i] = xn;
                 ss = fmaf(xn, xn, ss);
                 if (i >= p0 && i < p1) g.x_out[i] = xn;
@@ -700,10 +714,19 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((uint32_t)bytes) : "memory");
         }
     }
+    const bool racc = g.prologue == TEAL_PRO_RMS_ACC;
+    if (racc && g.xwait >= 0) {  // stage x before the wait (off the critical path)
+        wait_range(P.counters, g.xwait, g.xwait, g.xwait_target);
+        rms_stage_x(g, s);
+    }
     if (ph.dep_kind == TEAL_DEP_GLOBAL) wait_range(P.counters, ph.dep, ph.dep, ph.target);
     // PRO_RMSNORM: rden computed by the first compaction, overlapped with its x loads
     float rden = rms ? -1.f : 1.f;
-    if (g.prologue == TEAL_PRO_RMS_ACC) rden = rms_acc_prep(g, c, G, s);
+    if (racc) {
+        if (g.xwait < 0) rms_stage_x(g, s);
+        rden = rms_acc_finish(g, c, G, s);
+        if (g.xsig >= 0) signal(P.counters, g.xsig, g.xsig);  // x_out share written
+    }
     constexpr int ROWB = WFmt<WT>::ROWB;
     int segi = 0, lasts = 0;
 #define SL_STAMP(k, v) do { if (tl && tid == 0) tl[k] = (v); } while (0)

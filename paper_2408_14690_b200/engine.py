@@ -49,7 +49,8 @@ class StepGroup(ctypes.Structure):
                 ("prologue", c_i), ("nss", c_i), ("eps", c_f), ("epilogue", c_i),
                 ("nq", c_i), ("nkv", c_i), ("head_dim", c_i), ("kv_dtype", c_i), ("w_dtype", c_i),
                 ("gscale", c_vp), ("group", c_i), ("t_all", c_f), ("tile_stride_b", c_i64), ("row_stride_b", c_i64),
-                ("acc", c_vp), ("in_acc", c_vp), ("x_out", c_vp), ("ranges", c_vp), ("nranges", c_i), ("pad2_", c_i)]
+                ("acc", c_vp), ("in_acc", c_vp), ("x_out", c_vp), ("ranges", c_vp), ("nranges", c_i),
+                ("xsig", c_i), ("xwait", c_i), ("xwait_target", c_i), ("pad3_", c_i)]
 
 
 class StepAttn(ctypes.Structure):
@@ -446,12 +447,14 @@ class StepDecoder:
         Gc = self.grid
         nt_qkv, nt_o, nt_gu, nt_dn = (nq + 2 * nkv) // TW, d // TW, f // TH, d // TW
         # counters: 0 load; per layer: attn deps [KVH], ctx ready [KVH], o done, gate/up tiles [nt_gu], down done
-        per_layer = 2 * KVH + 1 + nt_gu + 1
+        # + x-ready counters of the two residual versions the layer materialises
+        per_layer = 2 * KVH + 1 + nt_gu + 1 + 2
         self.ncounters = 1 + per_layer * L
 
         def cbase(l):
             b = 1 + per_layer * l
-            return dict(attn=b, odep=b + KVH, odone=b + 2 * KVH, gu=b + 2 * KVH + 1, down=b + 2 * KVH + 1 + nt_gu)
+            return dict(attn=b, odep=b + KVH, odone=b + 2 * KVH, gu=b + 2 * KVH + 1, down=b + 2 * KVH + 1 + nt_gu,
+                        xq=b + 2 * KVH + 2 + nt_gu, xg=b + 2 * KVH + 3 + nt_gu)
 
         mc = {"qkv": max_contributors(nt_qkv, d, Gc), "o": max_contributors(nt_o, nq, Gc),
               "gu": max_contributors(nt_gu, d, Gc), "down": max_contributors(nt_dn, f, Gc)}
@@ -591,6 +594,26 @@ class StepDecoder:
             tab = self.range_tables[key]
             if tab is not None:
                 g.ranges, g.nranges = tab.data_ptr(), tab.shape[0]
+
+        def ctas_of(g):  # CTAs taking part in a GEMV group (each writes one x_out share)
+            return g.nranges if g.ranges else participants(g.ntiles, g.ntiles * (-(-g.m // 32)), Gc)
+
+        # x-ready counters: an RMS_ACC phase stages the previous residual version
+        # (complete once every CTA of its producer wrote its share) before waiting
+        # for its own accumulator.  Groups per layer: qkv, o, gate/up, down; then LM.
+        for l in range(L):
+            gq, gg = groups[4 * l], groups[4 * l + 2]
+            if l > 0:
+                gq.xsig = cbase(l)["xq"]
+                gq.xwait, gq.xwait_target = cbase(l - 1)["xg"], ctas_of(groups[4 * (l - 1) + 2])
+            gg.xsig = cbase(l)["xg"]
+            if l == 0:
+                gg.xwait, gg.xwait_target = 0, Gc  # xv[0]: the load phase
+            else:
+                gg.xwait, gg.xwait_target = cbase(l)["xq"], ctas_of(gq)
+        if spec.vocab:
+            gl = groups[4 * L]
+            gl.xwait, gl.xwait_target = cbase(L - 1)["xg"], ctas_of(groups[4 * (L - 1) + 2])
         self._keep = keep
         self._groups = dev_bytes((StepGroup * len(groups))(*groups))
         self._attns = dev_bytes((StepAttn * len(attns))(*attns))
@@ -650,6 +673,7 @@ class StepDecoder:
         g.nq, g.nkv, g.head_dim, g.kv_dtype = spec.n_q, spec.n_kv, spec.head_dim, RT.dtype_code(self.kv_dtype)
         g.w_dtype = wt.dtype_code
         g.acc, g.in_acc, g.x_out = RT.ptr(acc), RT.ptr(in_acc), RT.ptr(x_out)
+        g.xsig, g.xwait, g.xwait_target = -1, -1, 0
         return g
 
     # -- step -----------------------------------------------------------------
