@@ -82,6 +82,13 @@ struct Smem {
     int last;
 };
 constexpr size_t kSmemBytes = sizeof(Smem);
+// The CTA's shared memory seen through its declared address space: noinline
+// functions must not take Smem& parameters (the pointer would be generic and
+// every access a generic LD/ST instead of LDS/STS).
+__device__ __forceinline__ Smem& smem() {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    return *reinterpret_cast<Smem*>(smem_raw);
+}
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
@@ -211,8 +218,8 @@ __device__ __forceinline__ teal_step_tile tile_meta(const teal_step_group& g, in
 // ---- epilogue of one finished column tile (thread c = column c) --------------
 // `pre`: the residual value of this column, loaded by the caller together
 // with the split-K partials (RESID epilogue).
-__device__ __noinline__ void finalize(const teal_step_plan& P, const teal_step_group& g, int tile, float v, Smem& s,
-                                      float pre) {
+__device__ __noinline__ void finalize(const teal_step_plan& P, const teal_step_group& g, int tile, float v, float pre) {
+    Smem& s = smem();
     const int c = threadIdx.x;
     const int64_t col = (int64_t)tile * TW + c;
     const teal_step_tile tm = tile_meta(g, tile);
@@ -810,7 +817,7 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
             pre = __ldcg(g.resid + (int64_t)tile * TW + tid);
         }
         if (g.col_scale) v *= g.col_scale[(int64_t)tile * TW + tid];
-        finalize(P, g, tile, v, s, pre);
+        finalize(P, g, tile, v, pre);
         ++lasts;
         if (segi == 0) SL_STAMP(4, gtimer());
     }
@@ -838,8 +845,8 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
 // appends to the cache (rounded to the cache dtype first, as later steps will
 // read it).
 
-__device__ __noinline__ void attn_stage_kv(const teal_step_attn& a, int p0, int np, int newrow, int64_t kvbase,
-                                           Smem& s) {
+__device__ __noinline__ void attn_stage_kv(const teal_step_attn& a, int p0, int np, int newrow, int64_t kvbase) {
+    Smem& s = smem();
     constexpr int PER = ATT_STAGE / 16 / NT;  // n16 <= ATT_STAGE / 16 = PER * NT
     const int tid = threadIdx.x, hd = a.hd;
     const int kvb = a.kv_dtype == TEAL_BF16 ? 2 : 4;
@@ -863,8 +870,8 @@ __device__ __noinline__ void attn_stage_kv(const teal_step_attn& a, int p0, int 
     }
 }
 
-__device__ __noinline__ void attn_stage_q(const teal_step_attn& a, int g, int pos, int newrow, int64_t kvbase,
-                                          Smem& s) {
+__device__ __noinline__ void attn_stage_q(const teal_step_attn& a, int g, int pos, int newrow, int64_t kvbase) {
+    Smem& s = smem();
     constexpr int QPT = ATT_MAXG * ATT_MAXHD / NT;
     const int tid = threadIdx.x, G = a.H / a.KVH, hd = a.hd, half = hd >> 1;
     const bool acc = a.qkv_acc != nullptr;
@@ -935,8 +942,8 @@ __device__ __noinline__ void attn_stage_q(const teal_step_attn& a, int g, int po
     }
 }
 
-__device__ __noinline__ void attn_unit(const teal_step_plan& P, const teal_step_attn& a, int g, int ch, int L,
-                                       Smem& s) {
+__device__ __noinline__ void attn_unit(const teal_step_plan& P, const teal_step_attn& a, int g, int ch, int L) {
+    Smem& s = smem();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = a.H / a.KVH, hd = a.hd;
     const int p0 = ch * a.chunk;
@@ -950,10 +957,10 @@ __device__ __noinline__ void attn_unit(const teal_step_plan& P, const teal_step_
     ATT_STAMP(0);
     const int pos = L - 1;
     const int newrow = (a.qkv_acc && pos >= p0 && pos < p1) ? pos - p0 : -1;
-    if (np > 0) attn_stage_kv(a, p0, np, newrow, kvbase, s);
+    if (np > 0) attn_stage_kv(a, p0, np, newrow, kvbase);
     wait_range(P.counters, a.dep_base + g, a.dep_base + g, a.dep_target[g]);  // q / new row ready
     if (np > 0) {
-        attn_stage_q(a, g, pos, newrow, kvbase, s);
+        attn_stage_q(a, g, pos, newrow, kvbase);
         __syncthreads();
         ATT_STAMP(2);
         // scores: thread -> (head, position) pairs, 4 independent chains
@@ -1115,13 +1122,14 @@ __device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, S
     const int cr = G - 1 - (int)blockIdx.x;
     for (int u = (int)(((int64_t)cr * nu + G - 1) / G); u < nu && (int64_t)u * G / nu == cr; ++u) {
         const int g = u % a.KVH, ch = u / a.KVH;  // (the unit waits for its q/k/v tiles itself)
-        attn_unit(P, a, g, ch, L, s);
+        attn_unit(P, a, g, ch, L);
         __syncthreads();
     }
 }
 
 // ---- residual load: x = emb[token] (or x_in); ss partials; {pos, len} ---------
-__device__ __noinline__ void load_phase(const teal_step_plan& P, Smem& s) {
+__device__ __noinline__ void load_phase(const teal_step_plan& P) {
+    Smem& s = smem();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (P.acc_zero) {  // every CTA zeroes its share of this step's ACC accumulators (16 B stores)
         int4* z = reinterpret_cast<int4*>(P.acc_zero);
@@ -1196,7 +1204,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const __grid_constant__ 
         if (ph.kind == TEAL_PHASE_GEMV) gemv_slice_t<WT, UB>(P, ph, P.groups[ph.group], s, pol, tl);
         else if (ph.kind == TEAL_PHASE_ATTN) attn_phase(P, ph, s);
         else if (ph.kind == TEAL_PHASE_RESID) resid_phase(P, ph, P.groups[ph.group]);
-        else load_phase(P, s);
+        else load_phase(P);
         __syncthreads();
         if (tl && tid == 0) tl[1] = gtimer();
     }

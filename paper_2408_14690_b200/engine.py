@@ -640,8 +640,9 @@ class StepDecoder:
     def enable_timeline(self) -> torch.Tensor:
         """Debug: record %globaltimer at entry/exit of every phase of every CTA
         ([grid, nphases, 8] int64, overwritten by each launch): 0 start, 1 end;
-        GEMV phases also 2 deps met, 3/5 first/second segment streamed, 4 first
-        segment finished, 6 segments, 7 tiles this CTA finalized."""
+        GEMV phases also 2 prologue done (first segment's rows ready), 3/5
+        first/second segment streamed, 4 first segment finished, 6 segments,
+        7 global dependency met."""
         self.timeline = torch.zeros(self.grid, self.nphases, 8, device=self.device, dtype=torch.int64)
         self.plan.timeline = self.timeline.data_ptr()
         return self.timeline

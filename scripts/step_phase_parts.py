@@ -1,7 +1,12 @@
+"""Median-CTA composition of each GEMV phase of the persistent step (layers
+1-5 of an 8-layer Llama-3-8B-shaped model at s=0.5, 10 steps): poll = wait
+for the global dependency, prep = prologue (RMS finish / row deps),
+stream1 = compaction + streaming of the first segment, tail = reduction and
+signals; end_spread = latest minus median CTA end."""
 import sys
 from pathlib import Path
 import torch
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2408_14690_b200 import decode as D
 from paper_2408_14690_b200 import engine as E
 spec = D.DecoderSpec(4096, 32, 8, 14336, 8, vocab=128256, rope_theta=500000.0, norm_eps=1e-5, max_seq=2048)

@@ -38,7 +38,7 @@ for p in range(6, 12):
         ok = t[:, p, 2] > 0
         line += (f"\n      dep wait med {dep[ok].median():6.1f} max {dep[ok].max():6.1f} | seg1 stream med {s1[ok].median():6.1f} max {s1[ok].max():6.1f}"
                  f" | seg1 fin med {f1[ok].median():6.1f} max {f1[ok].max():6.1f} | 2-seg CTAs {int(two.sum())} seg2 med {s2[two].median() if two.any() else 0:6.1f}"
-                 f" | tail (last stream->end) med {tail[ok].median():6.1f} max {tail[ok].max():6.1f} | finalizers {int((t[:, p, 7] > 0).sum())}")
+                 f" | tail (last stream->end) med {tail[ok].median():6.1f} max {tail[ok].max():6.1f}")
         # the slowest CTA
         c = int(torch.argmax(t[:, p, 1]))
         row = ((t[c, p, :6] - t0) / 1e3).tolist()
