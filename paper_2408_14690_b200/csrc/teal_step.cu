@@ -435,7 +435,7 @@ __device__ void rms_stage_x(const teal_step_group& g, Smem& s) {
 
 __device__ float rms_acc_finish(const teal_step_group& g, int c, int G, Smem& s) {
     const int tid = threadIdx.x, m = g.m;
-    const int p0 = (int)((int64_t)c * m / G), p1 = (int)((int64_t)(c + 1) * m / G);
+    const int p0 = c * m / G, p1 = (c + 1) * m / G;  // m <= XS_MAX: 32-bit
     float ss = 0.f;
 #pragma unroll 1
     for (int i0 = 0; i0 < m; i0 += 16 * NT) {
@@ -472,8 +472,21 @@ __device__ __forceinline__ int participants(int ntiles, int64_t F) {
     return grid;
 }
 
+// a * b / c for non-negative operands; 32-bit division when the product fits
+// (every step-plan group), 64-bit (a software routine) only for huge
+// single-GEMV launches
+__device__ __forceinline__ int64_t muldiv(int64_t a, int64_t b, int64_t c) {
+    const int64_t p = a * b;
+    if (p <= 0x7fffffff && c <= 0x7fffffff) return (int64_t)((unsigned)p / (unsigned)c);
+    return p / c;
+}
+
 __device__ __forceinline__ int owner_of(int64_t gidx, int64_t F, int G) {
-    return (int)(((gidx + 1) * (int64_t)G - 1) / F);
+    const int64_t p = (gidx + 1) * (int64_t)G - 1;
+    return (int)((p <= 0x7fffffff && F <= 0x7fffffff) ? (int64_t)((unsigned)p / (unsigned)F) : p / F);
+}
+__device__ __forceinline__ int tile_of(int64_t gidx, int gpt) {
+    return gidx <= 0x7fffffff ? (int)((unsigned)gidx / (unsigned)gpt) : (int)(gidx / gpt);
 }
 
 // Threshold + compact rows [r0, r1) of one tile into s.u.g (ordered).
@@ -703,15 +716,15 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
     if (c >= G) return;
     int4 rg = make_int4(0, 0, 0, 0);
     if (g.ranges) rg = g.ranges[c];
-    const int64_t g0 = g.ranges ? (int64_t)rg.x : (int64_t)c * F / G;
-    const int64_t g1 = g.ranges ? (int64_t)rg.y : (int64_t)(c + 1) * F / G;
+    const int64_t g0 = g.ranges ? (int64_t)rg.x : muldiv(c, F, G);
+    const int64_t g1 = g.ranges ? (int64_t)rg.y : muldiv(c + 1, F, G);
     const bool rms = g.prologue == TEAL_PRO_RMSNORM || g.prologue == TEAL_PRO_RMS_ACC;
     // While this slice waits for its inputs, pull the head of its weight range
     // into L2 (one bulk prefetch of contiguous tiled rows): the wait is tail
     // time of the previous phase, when HBM is mostly idle.  Rows that turn out
     // pruned cost idle bandwidth only; kept rows then stream from L2.
     if (tid == 0 && P.prefetch_bytes > 0) {
-        const int tile = (int)(g0 / gpt);
+        const int tile = tile_of(g0, gpt);
         const int r0 = (int)(g0 - (int64_t)tile * gpt) * 32;
         const int r1 = min(g.m, (int)(min64(g1, (int64_t)(tile + 1) * gpt) - (int64_t)tile * gpt) * 32);
         const int64_t rowb = WFmt<WT>::ROWB;
@@ -738,7 +751,7 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
     int segi = 0, lasts = 0;
 #define SL_STAMP(k, v) do { if (tl && tid == 0) tl[k] = (v); } while (0)
     for (int64_t gs = g0; gs < g1; ++segi) {
-        const int tile = (int)(gs / gpt);
+        const int tile = tile_of(gs, gpt);
         const int64_t ge = min64(g1, (int64_t)(tile + 1) * gpt);
         const int r0 = (int)(gs - (int64_t)tile * gpt) * 32;
         const int r1 = min(g.m, (int)(ge - (int64_t)tile * gpt) * 32);
