@@ -372,14 +372,22 @@ __device__ __forceinline__ void unpack8(const LaneW<WT>& d, float w[8]) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) w[q] = __uint_as_float(d.u[q]);
     } else if constexpr (WT == TEAL_I8) {
+        // magic-number conversion (no I2F, a quarter-rate op): b ^ 0x80 = b + 128
+        // placed in the mantissa of 2^23 (one PRMT), minus 2^23 + 128 (one FADD)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) w[k] = (float)(int8_t)((d.u[k >> 2] >> (8 * (k & 3))) & 0xffu);
-    } else {
+        for (int q = 0; q < 2; ++q) {
+            const uint32_t x = d.u[q] ^ 0x80808080u;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int nib = (int)((d.u[0] >> (4 * k)) & 0xfu);
-            w[k] = (float)(nib >= 8 ? nib - 16 : nib);
+            for (int k = 0; k < 4; ++k)
+                w[4 * q + k] = __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7540u | k)) - 8388736.0f;
         }
+    } else {
+        // nibble n (two's complement) ^ 8 = n + 8 into the mantissa of 2^23
+        // (shift + LOP3), minus 2^23 + 8
+        const uint32_t x = d.u[0] ^ 0x88888888u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            w[k] = __uint_as_float(((x >> (4 * k)) & 0xfu) | 0x4B000000u) - 8388616.0f;
     }
 }
 
@@ -593,12 +601,15 @@ __device__ int compact_rows(const teal_step_group& g, const teal_step_tile& tm, 
 template <int WT, int UB>
 __device__ __forceinline__ void stream_rows(const unsigned char* tb, int64_t rsb, int cnt, const Smem& s, float acc[8],
                                             uint64_t pol, int gbase, int group, bool ok_lo, bool ok_hi) {
+    const int gsh = __ffs(group) - 1;  // int4 row groups: a power of two (host-checked)
     constexpr int ROWB = WFmt<WT>::ROWB;
     constexpr int LB = WFmt<WT>::LB;
     constexpr int HB = ROWB / 2;
     // rows per pipeline stage (int8 / int4 rows are narrower; measured: more
     // rows per stage does not help them — their unpack is issue-bound)
-    constexpr int U = WT == TEAL_F32 ? UB / 2 : UB;
+    // (narrow int8 / int4 rows: more of them per stage keep the bytes in
+    // flight per warp closer to bf16's, at similar register cost)
+    constexpr int U = WT == TEAL_F32 ? UB / 2 : (WT == TEAL_I8 ? UB + UB / 2 : (WT == TEAL_I4 ? 2 * UB : UB));
     constexpr int NW_ = LaneW<WT>::N;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int myhalf = lane < 16 ? 30 : 31;
@@ -652,7 +663,7 @@ __device__ __forceinline__ void stream_rows(const unsigned char* tb, int64_t rsb
     };
     auto flush_group = [&]() {  // int4: acc += accg * scale(group, column)
         if (curg >= 0) {
-            const float* sc = s.u.g.gsc + (curg - gbase / group) * TW + lane * 8;
+            const float* sc = s.u.g.gsc + (curg - (gbase >> gsh)) * TW + lane * 8;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 acc[j] = fmaf(accg[j], sc[j], acc[j]);
@@ -673,7 +684,7 @@ __device__ __forceinline__ void stream_rows(const unsigned char* tb, int64_t rsb
             } else if constexpr (WT == TEAL_I4) {
                 const int e = e0 + u;
                 if (e < cnt) {
-                    const int gr = (gbase + (int)((unsigned)s.u.g.idx[e] & 0x3fffffffu)) / group;
+                    const int gr = (gbase + (int)((unsigned)s.u.g.idx[e] & 0x3fffffffu)) >> gsh;
                     if (gr != curg) {
                         flush_group();
                         curg = gr;

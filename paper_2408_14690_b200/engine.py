@@ -241,6 +241,8 @@ class TiledW:
 def quantize_tiles(t: torch.Tensor, quant: str | None, group: int = 128) -> TiledW:
     """Quantise tiled weights [ntiles, m, TW]: None keeps the dtype; 'int8'
     symmetric per output column; 'int4' symmetric per (row group, column)."""
+    if quant == "int4" and (group < 128 or group & (group - 1)):
+        raise ValueError("int4 row groups must be a power of two >= 128")
     if quant is None:
         return TiledW(t.contiguous())
     w = t.float()
