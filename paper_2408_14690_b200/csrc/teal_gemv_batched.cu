@@ -66,14 +66,16 @@ __device__ __forceinline__ void unpack(const uint4 d, float* w) {
 #pragma unroll
         for (int k = 0; k < CPL; ++k) w[k] = (k & 1) ? bf16_hi(u[k >> 1]) : bf16_lo(u[k >> 1]);
     } else if constexpr (WT == TEAL_I8) {
+        // magic-number conversion (no quarter-rate I2F): b ^ 0x80 = b + 128 in
+        // the mantissa of 2^23 (PRMT), minus 2^23 + 128 (FADD)
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) w[k] = (float)(int8_t)((u[k >> 2] >> (8 * (k & 3))) & 0xffu);
+        for (int k = 0; k < CPL; ++k)
+            w[k] = __uint_as_float(__byte_perm(u[k >> 2] ^ 0x80808080u, 0x4B000000u, 0x7540u | (k & 3))) - 8388736.0f;
     } else {
+        // nibble n ^ 8 = n + 8 in the mantissa of 2^23, minus 2^23 + 8
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) {
-            const int nib = (int)((u[k >> 3] >> (4 * (k & 7))) & 0xfu);
-            w[k] = (float)(nib >= 8 ? nib - 16 : nib);
-        }
+        for (int k = 0; k < CPL; ++k)
+            w[k] = __uint_as_float((((u[k >> 3] ^ 0x88888888u) >> (4 * (k & 7))) & 0xfu) | 0x4B000000u) - 8388616.0f;
     }
 }
 
