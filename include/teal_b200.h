@@ -380,6 +380,11 @@ typedef struct teal_step_plan {
     int w_dtype, ctas;               /* ctas: grid size (<= resident capacity)  */
     long long* acc_zero;             /* LOAD: ACC accumulators zeroed each step */
     int64_t acc_zero_n;              /* (elements)                              */
+    int phase_begin, phase_end;      /* this launch runs phases [begin, end) (end 0: all).
+                                        Dependencies on earlier launches are met by stream
+                                        order: the host drops them from the phase list
+                                        (tensor parallel: an all-reduce of the row-parallel
+                                        accumulators between launches).                  */
 } teal_step_plan;
 
 /* Resident CTAs per SM of the step kernel for a weight dtype; the plan's

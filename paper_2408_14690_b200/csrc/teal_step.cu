@@ -1135,8 +1135,9 @@ __device__ __noinline__ void attn_unit(const teal_step_plan& P, const teal_step_
 __device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, Smem& s) {
     const teal_step_attn& a = P.attns[ph.group];
     // the sequence length is written by this step's load phase: a CTA that had
-    // no qkv slice reaches this point without having waited for it
-    wait_range(P.counters, 0, 0, (int)gridDim.x);
+    // no qkv slice reaches this point without having waited for it (the
+    // phase's GLOBAL dependency; none when the load ran in an earlier launch)
+    if (ph.dep_kind == TEAL_DEP_GLOBAL) wait_range(P.counters, ph.dep, ph.dep, ph.target);
     const int L = __ldcg(P.state + 1);
     const int nact = min(a.nchunks, (L + a.chunk - 1) / a.chunk);  // chunks holding positions
     const int nu = a.KVH * nact;
@@ -1221,7 +1222,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const __grid_constant__ 
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
     const int tid = threadIdx.x;
     const uint64_t pol = l2_evict_first_policy();
-    for (int p = 0; p < P.nphases; ++p) {
+    const int pend = P.phase_end > 0 ? P.phase_end : P.nphases;
+    for (int p = P.phase_begin; p < pend; ++p) {
         const teal_step_phase ph = P.phases[p];
         unsigned long long* tl = P.timeline ? P.timeline + ((int64_t)blockIdx.x * P.nphases + p) * 8 : nullptr;
         if (tl && tid == 0) tl[0] = gtimer();
@@ -1422,6 +1424,9 @@ int teal_step_launch(const teal_step_plan* p, cudaStream_t stream) {
     TEAL_REQUIRE(p && p->groups && p->phases && p->counters && p->ctrl && p->x && p->ss && p->state,
                  "teal_step_launch: null plan field");
     TEAL_REQUIRE(p->nphases >= 1 && p->ncounters >= 1, "teal_step_launch: empty plan");
+    TEAL_REQUIRE(p->phase_begin >= 0 && p->phase_end >= 0 && p->phase_end <= p->nphases &&
+                     (p->phase_end == 0 || p->phase_begin < p->phase_end),
+                 "teal_step_launch: bad phase range [%d, %d)", p->phase_begin, p->phase_end);
     TEAL_REQUIRE(!p->acc_zero || (p->acc_zero_n % 2 == 0 && (reinterpret_cast<uintptr_t>(p->acc_zero) & 15) == 0),
                  "teal_step_launch: acc_zero must be 16-byte aligned with an even element count");
     TEAL_REQUIRE(p->d >= TW && p->d % TW == 0, "teal_step_launch: d must be a multiple of %d", TW);

@@ -70,7 +70,7 @@ class StepPlan(ctypes.Structure):
                 ("cand_v", c_vp), ("cand_i", c_vp), ("token_out", c_vp), ("lm_done", c_vp), ("timeline", c_vp),
                 ("nphases", c_i), ("ncounters", c_i), ("prefetch_bytes", c_i), ("pad_", c_i),
                 ("d", c_i), ("emb_dtype", c_i), ("w_dtype", c_i), ("ctas", c_i),
-                ("acc_zero", c_vp), ("acc_zero_n", c_i64)]
+                ("acc_zero", c_vp), ("acc_zero_n", c_i64), ("phase_begin", c_i), ("phase_end", c_i)]
 
 
 PHASE_LOAD, PHASE_GEMV, PHASE_ATTN, PHASE_RESID = 0, 1, 2, 3
@@ -361,8 +361,9 @@ class StepDecoder:
         d, f, hd = spec.d_model, spec.d_ff, spec.head_dim
         nq, nkv, L = spec.n_q, spec.n_kv, spec.n_layers
         G = spec.n_heads // spec.n_kv_heads
-        if d % TW or nq % TW or nkv % TW or TW % hd or f % TH:
-            raise ValueError(f"StepDecoder needs d, n_q, n_kv multiples of {TW}, head_dim | {TW}, d_ff multiple of {TH}")
+        if d % TW or nq % TW or nkv % TH or (nq + 2 * nkv) % TW or TH % hd or f % TH:
+            raise ValueError(f"StepDecoder needs d, n_q multiples of {TW}, n_kv of {TH}, head_dim | {TH}, "
+                             f"d_ff multiple of {TH}")
         if d > XS_MAX:
             raise ValueError(f"StepDecoder needs d_model <= {XS_MAX}")
         if G > 8 or hd > 128 or G * hd > 1024:
@@ -475,6 +476,7 @@ class StepDecoder:
         def accs(l):
             b = self.acc[l * per_acc:(l + 1) * per_acc]
             return dict(o=b[:d], down=b[d:2 * d], gu=b[2 * d:2 * d + nt_gu * TW], qkv=b[2 * d + nt_gu * TW:])
+        self.acc_views = [accs(l) for l in range(L)]
         K_ = CONTRIB
 
         groups, attns, phases, keep = [], [], [], []
@@ -504,18 +506,22 @@ class StepDecoder:
             # --- qkv: RMSNorm(x) -> 3 thresholds -> q (RoPE), k (RoPE) -> cache, v -> cache
             meta, feeds = [], [0] * KVH
             for ti in range(nt_qkv):
-                c0, c1 = ti * TW, ti * TW + TW - 1
-                seg = 0 if c0 < nq else (1 if c0 < nq + nkv else 2)
-                first = c0 in (0, nq, nq + nkv)
-                if seg == 0:
-                    g0, g1 = (c0 // hd) // G, (c1 // hd) // G
-                else:
-                    off = nq if seg == 1 else nq + nkv
-                    g0, g1 = (c0 - off) // hd, (c1 - off) // hd
+                halves = []  # q / k / v segment per 128-column half (n_kv may be a multiple of 128)
+                for hh in range(2):
+                    c0 = ti * TW + hh * TH
+                    c1 = c0 + TH - 1
+                    seg = 0 if c0 < nq else (1 if c0 < nq + nkv else 2)
+                    if seg == 0:
+                        g0, g1 = (c0 // hd) // G, (c1 // hd) // G
+                    else:
+                        off = nq if seg == 1 else nq + nkv
+                        g0, g1 = (c0 - off) // hd, (c1 - off) // hd
+                    halves.append((seg, int(c0 in (0, nq, nq + nkv)), g0, g1))
+                (sl, fl, a0, a1), (sh, fh, b0, b1) = halves
+                g0, g1 = min(a0, b0), max(a1, b1)  # kv groups signalled by this tile
                 for gg in range(g0, g1 + 1):
                     feeds[gg] += 1
-                tv = _t32(t[seg])
-                meta.append(StepTile(tv, tv, seg, seg, int(first), int(first), cb["attn"] + g0, cb["attn"] + g1))
+                meta.append(StepTile(_t32(t[sl]), _t32(t[sh]), sl, sh, fl, fh, cb["attn"] + g0, cb["attn"] + g1))
             groups.append(self._group(tw["qkv"], tiles_tensor(meta), m=d, n=nq + 2 * nkv, maxc=mc["qkv"],
                                       gain=lw.rms_attn, ws="qkv", **qkv_in, acc=None if _NO_QKV_ACC else A["qkv"],
                                       epilogue=SEPI_QKV, q_out=self.q, k_cache=kc, v_cache=vc,
@@ -531,7 +537,7 @@ class StepDecoder:
                                   spec.n_heads, KVH, hd, RT.dtype_code(self.kv_dtype), self.attn_chunk,
                                   self.nchunks, cb["odep"], cb["attn"], tgt.data_ptr(), RT.ptr(self.attn_dbg),
                                   None if _NO_QKV_ACC else A["qkv"].data_ptr(), RT.ptr(self.rope_cos), RT.ptr(self.rope_sin), nq, nkv))
-            phases.append(StepPhase(PHASE_ATTN, len(attns) - 1, DEP_NONE, 0, 0, 1))
+            phases.append(StepPhase(PHASE_ATTN, len(attns) - 1, DEP_GLOBAL, 0, Gc, 1))  # step state from the load
             # --- o: rows = context channels, each waits for its kv group's context
             tv = _t32(t[3])
             meta = [StepTile(tv, tv, 0, 0, int(ti == 0), int(ti == 0), cb["odone"], cb["odone"]) for ti in range(nt_o)]
@@ -617,9 +623,11 @@ class StepDecoder:
             gl = groups[4 * L]
             gl.xwait, gl.xwait_target = cbase(L - 1)["xg"], ctas_of(groups[4 * (L - 1) + 2])
         self._keep = keep
-        self._groups = dev_bytes((StepGroup * len(groups))(*groups))
+        self._groups_host = (StepGroup * len(groups))(*groups)
+        self._phases_host = (StepPhase * len(phases))(*phases)
+        self._groups = dev_bytes(self._groups_host)
         self._attns = dev_bytes((StepAttn * len(attns))(*attns))
-        self._phases = dev_bytes((StepPhase * len(phases))(*phases))
+        self._phases = dev_bytes(self._phases_host)
         self.nphases = len(phases)
         self.counters = torch.zeros(self.ncounters * 32, device=dev, dtype=torch.int32)
         self.ctrl = torch.zeros(4, device=dev, dtype=torch.int32)
@@ -638,6 +646,11 @@ class StepDecoder:
         p.w_dtype, p.ctas = self.w_code, self.grid
         p.prefetch_bytes = self.prefetch_bytes
         self.plan = p
+
+    def _upload_plan(self) -> None:
+        """Re-upload the (host-edited) group and phase tables."""
+        for t, h in ((self._groups, self._groups_host), (self._phases, self._phases_host)):
+            t.copy_(torch.frombuffer(bytearray(bytes(h)), dtype=torch.uint8))
 
     def enable_timeline(self) -> torch.Tensor:
         """Debug: record %globaltimer at entry/exit of every phase of every CTA

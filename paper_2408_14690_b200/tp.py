@@ -179,3 +179,141 @@ def run_lockstep(decs, from_token: bool = True, stream_h: int | None = None) -> 
             full = torch.cat([o[2] for o in ops])
             for o in ops:
                 o[1].copy_(full)
+
+
+# ---- tensor parallelism on the persistent step engine ---------------------------
+class TPStepDecoder:
+    """One rank of a tensor-parallel decode on the persistent step kernel
+    (engine.StepDecoder over this rank's weight shard, :func:`shard_weights`).
+
+    The row-parallel o / down projections already reduce their split-K
+    partials into int64 fixed-point accumulators (2^-32 units) that the next
+    phase's prologue adds to the residual stream.  Tensor parallelism is then
+    one integer-sum all-reduce of those accumulators per row-parallel
+    projection, between two launches of the step kernel's phase list:
+
+        launch [load, qkv0, attn0, o0]   all-reduce acc_o[0]
+        launch [gu0, down0]              all-reduce acc_down[0]
+        launch [qkv1, attn1, o1]         all-reduce acc_o[1]  ...
+        launch [lm]                      all-gather the per-tile argmax candidates
+
+    Integer addition is exact and associative, so every rank holds the same
+    sums whatever the reduction order (NCCL ring / tree / NVLS), and the
+    replicated residual stream stays bit-identical across ranks.  Column-
+    parallel q/k/v/gate/up masks are computed on the replicated residual
+    (identical on every rank); row-parallel masks are rank-local (each rank
+    thresholds its own heads' context / its d_ff slice).  Dependencies that
+    cross a launch boundary are dropped from the phase list (stream order
+    meets them)."""
+
+    def __init__(self, shard: DecoderWeights, thresholds=None, rank: int = 0, world: int = 1,
+                 full_vocab: int = 0, **kw):
+        from . import engine as E
+        self.E = E
+        self.rank, self.world = rank, world
+        self.dec = E.StepDecoder(shard, thresholds, **kw)
+        d = self.dec
+        self.spec = d.spec
+        self.vocab_local = d.spec.vocab
+        self.full_vocab = full_vocab or self.vocab_local * world
+        L = d.spec.n_layers
+        lm = 1 if d.spec.vocab else 0
+        # phase indices: 0 load; layer l: qkv 1+5l, attn 2+5l, o 3+5l, gu 4+5l, down 5+5l; lm 1+5L
+        segs = []
+        for l in range(L):
+            segs.append((0 if l == 0 else 1 + 5 * l, 4 + 5 * l, ("o", l)))
+            segs.append((4 + 5 * l, 6 + 5 * l, ("down", l)))
+        if lm:
+            segs.append((1 + 5 * L, 2 + 5 * L, ("lm", None)))
+        self.segments = segs
+        # drop cross-launch dependencies (phases and x-ready waits)
+        ph, gr = d._phases_host, d._groups_host
+        for (b, _, _) in segs:
+            if b != 0:
+                ph[b].dep_kind = E.DEP_NONE
+        for l in range(1, L):
+            ph[2 + 5 * l].dep_kind = E.DEP_NONE  # attention: the load ran in the first launch
+        for gi in range(len(gr)):
+            gr[gi].xwait = -1
+        d._upload_plan()
+        self.token = d.token
+        if lm:
+            nt = d.lm_t.ntiles
+            self.cand_all_v = torch.empty(world * nt, device=d.device)
+            self.cand_all_i = torch.empty(world * nt, device=d.device, dtype=torch.int32)
+
+    def reset(self, start_pos: int = 0) -> None:
+        self.dec.reset(start_pos)
+
+    @property
+    def x(self):
+        return self.dec.x
+
+    def step_ops(self, stream_h: int, from_token: bool = True):
+        """Generator over one decode step: launches this rank's kernel
+        segments on `stream_h` and yields ('allreduce', int64 tensor) /
+        ('allgather', out_v, in_v, out_i, in_i) at every collective point."""
+        d, C = self.dec, self.E.C
+        L = C.lib()
+        p = d.plan
+        p.emb = d.w.embedding.data_ptr() if from_token else None
+        for (b, e, (kind, l)) in self.segments:
+            p.phase_begin, p.phase_end = b, e
+            C.check(L.teal_step_launch(ctypes.byref(p), stream_h))
+            if kind in ("o", "down"):
+                yield ("allreduce", d.acc_views[l][kind])
+            else:
+                yield ("allgather", self.cand_all_v, d.cand_v, self.cand_all_i, d.cand_i)
+                self._global_argmax()
+        p.phase_begin, p.phase_end = 0, 0
+
+    def _global_argmax(self) -> None:
+        # candidates in rank-major order = ascending vocabulary index, so the
+        # first maximum is the lowest index among ties (the kernel's rule)
+        nt = self.dec.cand_v.numel()
+        offs = (torch.arange(self.world, device=self.cand_all_i.device, dtype=torch.int32)
+                .repeat_interleave(nt) * self.vocab_local)
+        j = torch.argmax(self.cand_all_v)
+        self.token.copy_((self.cand_all_i[j] + offs[j]).reshape(1))
+
+
+def run_step_dist_step(dec: TPStepDecoder, from_token: bool = True, group=None) -> None:
+    """One step of a TPStepDecoder rank with torch.distributed collectives
+    (NCCL over NVLink: int64 SUM all-reduce of the accumulators)."""
+    import torch.distributed as dist
+    for op in dec.step_ops(RT.stream_handle(), from_token):
+        if op[0] == "allreduce":
+            dist.all_reduce(op[1], group=group)
+        else:
+            dist.all_gather_into_tensor(op[1], op[2].contiguous(), group=group)
+            dist.all_gather_into_tensor(op[3], op[4].contiguous(), group=group)
+
+
+def run_lockstep_step(decs, from_token: bool = True, stream_h: int | None = None) -> None:
+    """All ranks of a TPStepDecoder group on one device in lockstep: the
+    all-reduce is an int64 sum (exact), the all-gather a concatenation."""
+    sh = RT.stream_handle() if stream_h is None else stream_h
+    gens = [d.step_ops(sh, from_token) for d in decs]
+    while True:
+        ops = []
+        for g in gens:
+            try:
+                ops.append(next(g))
+            except StopIteration:
+                ops.append(None)
+        if all(o is None for o in ops):
+            return
+        if any(o is None for o in ops):
+            raise RuntimeError("tensor-parallel ranks diverged")
+        if ops[0][0] == "allreduce":
+            total = ops[0][1].clone()
+            for o in ops[1:]:
+                total += o[1]
+            for o in ops:
+                o[1].copy_(total)
+        else:
+            vs = torch.cat([o[2] for o in ops])
+            is_ = torch.cat([o[4] for o in ops])
+            for o in ops:
+                o[1].copy_(vs)
+                o[3].copy_(is_)

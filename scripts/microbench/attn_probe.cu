@@ -11,18 +11,16 @@ void set_error(const char*, ...) {}
 int check_launch(const char*) { return 0; }
 }
 
-__global__ void __launch_bounds__(NT, 1) probe(const __grid_constant__ teal_step_plan P, int reps) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+__global__ void __launch_bounds__(NT, 2) probe(const __grid_constant__ teal_step_plan P, int reps, int L) {
     for (int r = 0; r < reps; ++r) {
-        attn_unit_t<uint16_t>(P, P.attns[0], 0, 0, s);
+        attn_unit(P, P.attns[0], 0, 0, L);
         __syncthreads();
     }
 }
 
 int main() {
     const int H = 32, KVH = 8, hd = 128, max_seq = 2048, G = H / KVH;
-    for (int L : {16, 64, 256}) {
+    for (int L : {16, 41, 64}) {
         float *q, *ctx, *part;
         uint16_t *kc, *vc;
         int *state, *counters, *dep;
@@ -49,7 +47,7 @@ int main() {
         cudaMemset(dbg, 0, 4096);
         teal_step_attn a = {};
         a.q = q; a.k_cache = kc; a.v_cache = vc; a.ctx = ctx; a.partials = part; a.tickets = tickets;
-        a.max_seq = max_seq; a.H = H; a.KVH = KVH; a.hd = hd; a.kv_dtype = TEAL_BF16; a.chunk = 256; a.nchunks = max_seq / 256;
+        a.max_seq = max_seq; a.H = H; a.KVH = KVH; a.hd = hd; a.kv_dtype = TEAL_BF16; a.chunk = 64; a.nchunks = max_seq / 64;
         a.sig_base = 10; a.dep_base = 0; a.dep_target = dep; a.dbg = dbg;
         teal_step_attn* da;
         cudaMalloc(&da, sizeof(a));
@@ -57,11 +55,11 @@ int main() {
         teal_step_plan P = {};
         P.attns = da; P.state = state; P.counters = counters;
         cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
-        probe<<<1, NT, sizeof(Smem)>>>(P, 3);
+        probe<<<1, NT, sizeof(Smem)>>>(P, 3, L);
         cudaDeviceSynchronize();
         unsigned long long h[6];
         cudaMemcpy(h, dbg, 48, cudaMemcpyDeviceToHost);
-        printf("L=%4d (chunk 256, 1 CTA, 3rd rep): stage %.2f us, scores %.2f us, softmax+V+store %.2f us, signal %.2f us  err=%s\n", L,
+        printf("L=%4d (chunk 64, 1 CTA, 3rd rep): stage %.2f us, scores %.2f us, softmax+V+store %.2f us, signal %.2f us  err=%s\n", L,
                (h[2] - h[0]) / 1e3, (h[1] - h[2]) / 1e3, (h[4] - h[1]) / 1e3, (h[5] - h[4]) / 1e3, cudaGetErrorString(cudaGetLastError()));
     }
     return 0;

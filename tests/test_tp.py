@@ -145,3 +145,55 @@ def test_lockstep_tp_matches_single_gpu(world):
             assert rel_err(d.x.cpu().numpy(), ref.x.cpu().numpy()) < 1e-4
             assert rel_err(d.logits_full.cpu().numpy(), ref.logits.cpu().numpy()) < 1e-3
             assert int(d.token.item()) == int(ref.token.item())
+
+
+def _tp_spec():
+    from paper_2408_14690_b200 import decode as D
+    # n_kv = 4 heads x 128: TP 4 leaves one kv head (128 columns) per rank
+    return D.DecoderSpec(1024, 8, 4, 2048, 2, vocab=1024, rope_theta=500000.0, norm_eps=1e-5, max_seq=64)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_step_engine_tp_lockstep_matches_single_gpu(world):
+    # persistent step kernel per rank; the row-parallel o/down accumulators
+    # are summed (int64, exact) between launches; vocab-parallel argmax.
+    # fp32 KV cache: the TP and single-GPU split-K partials differ by ~1e-7
+    # (different CTA splits), which a bf16 cache can turn into one-ulp (4e-3)
+    # steps of single elements and from there into threshold flips; with an
+    # fp32 cache the two agree to ~1e-7 at every step.
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200 import engine as E
+    from paper_2408_14690_b200 import tp
+    from conftest import rel_err
+    spec = _tp_spec()
+    W = D.random_weights(spec, torch.bfloat16, seed=12)
+    thr = [[0.3, 0.4, 0.5, 0.02, 0.6, 0.7, 0.05]] * 2
+    ref = E.StepDecoder(W, thr, kv_dtype=torch.float32)
+    ranks = [tp.TPStepDecoder(tp.shard_weights(W, r, world), thr, rank=r, world=world, kv_dtype=torch.float32)
+             for r in range(world)]
+    ref.reset()
+    for d in ranks:
+        d.reset()
+    for tok in [5, 17, 999, 3, 250, 7, 7, 42, 11]:
+        ref.token.fill_(tok)
+        ref.step_token()
+        for d in ranks:
+            d.token.fill_(tok)
+        tp.run_lockstep_step(ranks)
+        torch.cuda.synchronize()
+        x0 = ranks[0].x.clone()
+        for d in ranks:
+            assert torch.equal(d.x, x0)  # replicated residual bit-identical across ranks
+            assert int(d.token.item()) == int(ref.token.item())
+        assert rel_err(x0.cpu().numpy(), ref.x.cpu().numpy()) < 1e-5
+
+
+def test_tp_step_shard_shapes_70b():
+    # Llama-3-70B at TP 8: 8 q heads + 1 kv head per rank fits the step
+    # engine's tiling (n_kv a multiple of 128 columns)
+    from paper_2408_14690_b200 import tp
+    from paper_2408_14690_b200.decode import LLAMA3_70B
+    ls = tp.shard_spec(LLAMA3_70B, 8)
+    assert ls.n_q % 256 == 0 and ls.n_kv % 128 == 0 and (ls.n_q + 2 * ls.n_kv) % 256 == 0
+    assert ls.d_ff % 128 == 0 and ls.d_model % 256 == 0
