@@ -278,15 +278,27 @@ class TPStepDecoder:
 
 
 def run_step_dist_step(dec: TPStepDecoder, from_token: bool = True, group=None) -> None:
-    """One step of a TPStepDecoder rank with torch.distributed collectives
-    (NCCL over NVLink: int64 SUM all-reduce of the accumulators)."""
+    """One step of a TPStepDecoder rank with torch.distributed collectives:
+    NCCL over NVLink (int64 SUM all-reduce of the accumulators, stream-
+    ordered), or any other backend through host copies (gloo tests)."""
     import torch.distributed as dist
+    nccl = dist.get_backend(group) == "nccl"
     for op in dec.step_ops(RT.stream_handle(), from_token):
         if op[0] == "allreduce":
-            dist.all_reduce(op[1], group=group)
+            if nccl:
+                dist.all_reduce(op[1], group=group)
+            else:
+                h = op[1].cpu()
+                dist.all_reduce(h, group=group)
+                op[1].copy_(h)
         else:
-            dist.all_gather_into_tensor(op[1], op[2].contiguous(), group=group)
-            dist.all_gather_into_tensor(op[3], op[4].contiguous(), group=group)
+            for out, inp in ((op[1], op[2]), (op[3], op[4])):
+                if nccl:
+                    dist.all_gather_into_tensor(out, inp.contiguous(), group=group)
+                else:
+                    parts = [torch.empty_like(inp, device="cpu") for _ in range(dist.get_world_size(group))]
+                    dist.all_gather(parts, inp.cpu(), group=group)
+                    out.copy_(torch.cat(parts))
 
 
 def run_lockstep_step(decs, from_token: bool = True, stream_h: int | None = None) -> None:

@@ -197,3 +197,63 @@ def test_tp_step_shard_shapes_70b():
     ls = tp.shard_spec(LLAMA3_70B, 8)
     assert ls.n_q % 256 == 0 and ls.n_kv % 128 == 0 and (ls.n_q + 2 * ls.n_kv) % 256 == 0
     assert ls.d_ff % 128 == 0 and ls.d_model % 256 == 0
+
+
+def _step_dist_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2408_14690_b200 import decode as D
+        from paper_2408_14690_b200 import engine as E
+        from paper_2408_14690_b200 import tp
+        torch.cuda.set_device(0)
+        spec = _tp_spec()
+        W = D.random_weights(spec, torch.bfloat16, seed=12)
+        thr = [[0.3, 0.4, 0.5, 0.02, 0.6, 0.7, 0.05]] * 2
+        dec = tp.TPStepDecoder(tp.shard_weights(W, rank, world), thr, rank=rank, world=world,
+                               kv_dtype=torch.float32)
+        dec.reset()
+        xs, toks = [], []
+        for tok in [5, 17, 999, 3]:
+            dec.token.fill_(tok)
+            tp.run_step_dist_step(dec)
+            torch.cuda.synchronize()
+            xs.append(dec.x.cpu().numpy().copy())
+            toks.append(int(dec.token.item()))
+        q.put((rank, xs, toks))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_step_engine_tp_torch_distributed_world2():
+    # two processes on one GPU (their cooperative launches time-slice), the
+    # collectives through torch.distributed (gloo here, NCCL on a multi-GPU box)
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200 import engine as E
+    from conftest import rel_err
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_step_dist_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=540) for _ in procs], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    spec = _tp_spec()
+    W = D.random_weights(spec, torch.bfloat16, seed=12)
+    thr = [[0.3, 0.4, 0.5, 0.02, 0.6, 0.7, 0.05]] * 2
+    ref = E.StepDecoder(W, thr, kv_dtype=torch.float32)
+    ref.reset()
+    for i, tok in enumerate([5, 17, 999, 3]):
+        ref.token.fill_(tok)
+        ref.step_token()
+        torch.cuda.synchronize()
+        for r in res:
+            assert r[2][i] == int(ref.token.item())
+            assert rel_err(r[1][i], ref.x.cpu().numpy()) < 1e-5
+        assert np.array_equal(res[0][1][i], res[1][1][i])
