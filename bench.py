@@ -74,6 +74,10 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--engine", choices=["step", "launch"], default="step")
+    ap.add_argument("--tp", action="store_true",
+                    help="config 4: tensor-parallel decode over the N ranks (persistent step kernel per rank, "
+                         "NCCL int64 all-reduce of the row-parallel accumulators) instead of N replicas")
+    ap.add_argument("--tp-model", choices=["8b", "70b"], default="70b")
     return ap.parse_args()
 
 
@@ -505,10 +509,115 @@ def run_ours(args):
     return 0
 
 
+def run_tp(args):
+    """Config 4: one token stream decoded by N GPUs (strong scaling).  Each
+    rank holds its shard (column-parallel q/k/v/gate/up/LM head, row-parallel
+    o/down) as random-init tiled weights; thresholds are calibrated on rank
+    0's shard and broadcast.  A step = 2 L + 1 launches of the rank's step
+    kernel and 2 L NCCL all-reduces of d int64 accumulators (+ one all-gather
+    of the LM-head argmax candidates)."""
+    import torch
+    ws, rank, local = dist_setup()
+    import paper_2408_14690_b200 as T  # noqa: F401
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200 import engine as E
+    from paper_2408_14690_b200 import tp
+    spec = D.LLAMA3_70B if args.tp_model == "70b" else D.LLAMA3_8B
+    ls = tp.shard_spec(spec, ws)
+    W = E.random_tiled_model(ls, torch.bfloat16, seed=rank)
+    thr_t = torch.zeros(spec.n_layers, 7, dtype=torch.float64, device="cuda")
+    if rank == 0:
+        hists = D.calibrate_histograms(W, n_tokens=8, engine="step")
+        thr_t.copy_(torch.tensor(D.uniform_thresholds(hists, spec.n_layers, args.sparsity), dtype=torch.float64))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.broadcast(thr_t, 0)
+    thr = thr_t.cpu().tolist()
+    dec = tp.TPStepDecoder(W, thr, rank=rank, world=ws, full_vocab=spec.vocab, count_kept=True)
+
+    def step():
+        if ws > 1:
+            tp.run_step_dist_step(dec)
+        else:
+            tp.run_lockstep_step([dec])
+
+    dec.reset()
+    dec.token.fill_(1)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # one CUDA graph per step (2 L + 1 kernel launches and the collectives;
+    # NCCL is graph-capturable): no host launch overhead between segments
+    eager = step
+    try:
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(g, stream=st):
+                eager()
+        torch.cuda.current_stream().wait_stream(st)
+        step = g.replay
+        graphed = True
+    except Exception as e:  # keep the eager path (reported in config)
+        print(f"[bench --tp] graph capture failed ({e}); timing eager steps", file=sys.stderr)
+        graphed = False
+    dec.reset()
+    dec.token.fill_(1)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dec.dec.kept.zero_()
+    pos0 = int(dec.dec.state[1].item())
+    with ClockSampler(local) as clk:
+        ms = timed(step, args.steps, ws)
+    value = args.steps * 1e3 / ms  # one token stream: tokens/s of the whole TP group
+    positions = sum(pos0 + i + 1 for i in range(args.steps))
+    algo = dec.dec.algorithmic_bytes(dec.dec.kept, steps=args.steps, positions=positions) / args.steps
+    gbs = algo / (ms / args.steps * 1e-3) / 1e9
+    # e2e: token H2D in, argmax D2H out every step
+    tin = torch.ones(1, dtype=torch.int32).pin_memory()
+    tout = torch.zeros(1, dtype=torch.int32).pin_memory()
+
+    def step_host():
+        dec.token.copy_(tin, non_blocking=True)
+        step()
+        tout.copy_(dec.token, non_blocking=True)
+
+    ms_e2e = timed(step_host, args.steps, ws)
+    peak, peak_src = peak_hbm()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"llama3-{args.tp_model} random-init batch-1 decode, tensor parallel",
+                       "sparsity": args.sparsity, "batch": 1, "parallelism": f"tp{ws}",
+                       "collective": "NCCL int64 all-reduce of row-parallel accumulators" if ws > 1 else "none",
+                       "cuda_graph": graphed,
+                       "l2": "inputs larger than L2"},
+            "roofline": {"bound": "hbm", "kernel": "teal step_kernel per rank (algorithmic bytes of rank 0 / step time)",
+                         "achieved": round(gbs, 1), "peak": peak, "peak_src": peak_src, "unit": "GB/s",
+                         "frac": round(gbs / peak, 4), "traffic": None},
+            "cpu_baseline": None,
+            "e2e": {"value": round(args.steps * 1e3 / ms_e2e, 2), "unit": UNIT, "h2d_bytes_per_step": 4,
+                    "d2h_bytes_per_step": 4},
+            "gpu_launches": (2 * spec.n_layers + 1) * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.tp:
+        return run_tp(args)
     return run_ours(args)
 
 

@@ -241,6 +241,8 @@ class TPStepDecoder:
             nt = d.lm_t.ntiles
             self.cand_all_v = torch.empty(world * nt, device=d.device)
             self.cand_all_i = torch.empty(world * nt, device=d.device, dtype=torch.int32)
+            self.cand_offs = (torch.arange(world, device=d.device, dtype=torch.int32)
+                              .repeat_interleave(nt) * self.vocab_local)
 
     def reset(self, start_pos: int = 0) -> None:
         self.dec.reset(start_pos)
@@ -270,11 +272,9 @@ class TPStepDecoder:
     def _global_argmax(self) -> None:
         # candidates in rank-major order = ascending vocabulary index, so the
         # first maximum is the lowest index among ties (the kernel's rule)
-        nt = self.dec.cand_v.numel()
-        offs = (torch.arange(self.world, device=self.cand_all_i.device, dtype=torch.int32)
-                .repeat_interleave(nt) * self.vocab_local)
-        j = torch.argmax(self.cand_all_v)
-        self.token.copy_((self.cand_all_i[j] + offs[j]).reshape(1))
+        # (no host synchronisation: the step is CUDA-graph capturable)
+        j = torch.argmax(self.cand_all_v).reshape(1)
+        self.token.copy_(torch.index_select(self.cand_all_i, 0, j) + torch.index_select(self.cand_offs, 0, j))
 
 
 def run_step_dist_step(dec: TPStepDecoder, from_token: bool = True, group=None) -> None:
