@@ -324,7 +324,10 @@ typedef struct teal_step_group {
     int xwait, xwait_target; /* PRO_RMS_ACC: x (the previous version) is complete when
                                 counters[xwait] >= xwait_target; it is then staged before
                                 the phase's own dependency wait (-1: stage after it)   */
-    int pad3_;
+    int tp_sum;              /* tensor parallel (plan.tp != NULL): a row-parallel ACC output —
+                                every contributor adds its partials to EVERY rank's
+                                accumulator and bumps every rank's tile counters (the
+                                consumers' targets are world x CONTRIB per tile)        */
 } teal_step_group;
 
 typedef struct teal_step_attn {
@@ -355,6 +358,24 @@ typedef struct teal_step_phase {
     int target, dep_rows;
 } teal_step_phase;
 
+/* Tensor-parallel group of a fused step launch (one launch per rank per
+ * token; peers reached through peer-mapped pointers — CUDA IPC / NVLink — or,
+ * for single-GPU validation, other ranks' buffers on the same device). */
+#define TEAL_TP_MAX 8
+typedef struct teal_step_tp {
+    long long* acc[TEAL_TP_MAX];      /* each rank's accumulator block (same layout)        */
+    int* counters[TEAL_TP_MAX];       /* each rank's dependency counters                   */
+    unsigned* epoch[TEAL_TP_MAX];     /* each rank's [world] completed-step counts; rank j
+                                         writes entry j of every rank's array at exit       */
+    int* token[TEAL_TP_MAX];          /* each rank's token word                            */
+    float* cand_v;                    /* rank 0: LM argmax candidates [world * ntiles]      */
+    int* cand_i;
+    unsigned* lm_ticket;              /* rank 0: LM tiles finished over all ranks          */
+    int world, rank;
+    int vocab_off;                    /* this rank's first vocabulary index                */
+    int pad_;
+} teal_step_tp;
+
 typedef struct teal_step_plan {
     const teal_step_group* groups;   /* device arrays */
     const teal_step_attn* attns;
@@ -380,6 +401,9 @@ typedef struct teal_step_plan {
     int w_dtype, ctas;               /* ctas: grid size (<= resident capacity)  */
     long long* acc_zero;             /* LOAD: ACC accumulators zeroed each step */
     int64_t acc_zero_n;              /* (elements)                              */
+    const teal_step_tp* tp;          /* nullable device pointer: fused tensor parallel     */
+    int noncoop, pad4_;              /* 1: ordinary launch (single-GPU TP validation runs the
+                                        ranks' launches concurrently on one device)       */
     int phase_begin, phase_end;      /* this launch runs phases [begin, end) (end 0: all).
                                         Dependencies on earlier launches are met by stream
                                         order: the host drops them from the phase list

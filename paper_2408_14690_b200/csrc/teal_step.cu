@@ -90,6 +90,12 @@ __device__ __forceinline__ Smem& smem() {
     return *reinterpret_cast<Smem*>(smem_raw);
 }
 
+__device__ __forceinline__ unsigned long long gtimer_() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -99,6 +105,31 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // Each counter lives in its own 128-byte line (index * CSTRIDE) so hundreds
 // of pollers of one counter do not contend with the other counters' updates.
 constexpr int CSTRIDE = 32;
+
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+    int v;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_sys(int* p, int v) {
+    asm volatile("red.release.sys.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Counters signalled by other GPUs (fused tensor parallel): system-scope
+// acquire, and a watchdog — a wait that cannot complete (a peer that never
+// launched) traps after ~10 s instead of hanging the device.
+__device__ __noinline__ void wait_range_sys(const int* counters, int c0, int c1, int target) {
+    if (threadIdx.x == 0) {
+        const unsigned long long t0 = gtimer_();
+        for (int c = c0; c <= c1; ++c) {
+            while (ld_acquire_sys(counters + (int64_t)c * CSTRIDE) < target) {
+                __nanosleep(128);
+                if (gtimer_() - t0 > 10000000000ull) asm volatile("trap;");
+            }
+        }
+    }
+    __syncthreads();
+}
 
 // thread 0 polls with backoff; the barrier publishes the result to the CTA
 __device__ __forceinline__ void wait_range(const int* counters, int c0, int c1, int target) {
@@ -296,21 +327,36 @@ __device__ __noinline__ void finalize(const teal_step_plan& P, const teal_step_g
                     if (s.scr[w] > tv || (s.scr[w] == tv && s.wcnt[w] < ti)) { tv = s.scr[w]; ti = s.wcnt[w]; }
                 P.cand_v[tile] = tv;
                 P.cand_i[tile] = ti;
-                __threadfence();
-                const unsigned prev = atomicAdd(P.lm_done, 1u);
-                s.last = prev == (unsigned)g.ntiles - 1u;
-                if (s.last) {
-                    *P.lm_done = 0u;
+                if (P.tp) {  // vocabulary-parallel: candidates and ticket on rank 0, global indices
+                    const teal_step_tp& T = *P.tp;
+                    const int slot = T.rank * g.ntiles + tile;
+                    T.cand_v[slot] = tv;
+                    T.cand_i[slot] = ti == 0x7fffffff ? ti : ti + T.vocab_off;
+                    __threadfence_system();
+                    unsigned prev;
+                    asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(T.lm_ticket) : "memory");
+                    s.last = prev == (unsigned)(T.world * g.ntiles) - 1u;
+                    if (s.last) *T.lm_ticket = 0u;
+                } else {
                     __threadfence();
+                    const unsigned prev = atomicAdd(P.lm_done, 1u);
+                    s.last = prev == (unsigned)g.ntiles - 1u;
+                    if (s.last) {
+                        *P.lm_done = 0u;
+                        __threadfence();
+                    }
                 }
             }
             __syncthreads();
             if (s.last) {  // the last tile: argmax over the per-tile candidates, whole CTA
                 float gv = -INFINITY;
                 int gi = 0x7fffffff;
-                for (int t = c; t < g.ntiles; t += NT) {
-                    const float cv = __ldcg(P.cand_v + t);
-                    const int ci = __ldcg(P.cand_i + t);
+                const float* cvs = P.tp ? P.tp->cand_v : P.cand_v;
+                const int* cis = P.tp ? P.tp->cand_i : P.cand_i;
+                const int ncand = P.tp ? P.tp->world * g.ntiles : g.ntiles;
+                for (int t = c; t < ncand; t += NT) {
+                    const float cv = __ldcg(cvs + t);
+                    const int ci = __ldcg(cis + t);
                     if (cv > gv || (cv == gv && ci < gi)) { gv = cv; gi = ci; }
                 }
 #pragma unroll
@@ -328,7 +374,11 @@ __device__ __noinline__ void finalize(const teal_step_plan& P, const teal_step_g
                             s.scr[0] = s.scr[w];
                             s.wcnt[0] = s.wcnt[w];
                         }
-                    *P.token_out = s.wcnt[0] == 0x7fffffff ? 0 : s.wcnt[0];
+                    const int tok = s.wcnt[0] == 0x7fffffff ? 0 : s.wcnt[0];
+                    if (P.tp)
+                        for (int j = 0; j < P.tp->world; ++j) *P.tp->token[j] = tok;
+                    else
+                        *P.token_out = tok;
                 }
             }
             __syncthreads();
@@ -716,6 +766,23 @@ __device__ __forceinline__ void stream_rows(const unsigned char* tb, int64_t rsb
     if constexpr (WT == TEAL_I4) flush_group();
 }
 
+// Fused tensor-parallel row-parallel output: this CTA's column partial goes
+// into every rank's accumulator (peer memory) and every rank's counters are
+// bumped (system-scope release after the CTA's adds).  Integer adds: the
+// sum is the same on every rank whatever the arrival order.
+__device__ __noinline__ void tp_accumulate(const teal_step_plan& P, const teal_step_group& g, int tile, long long fx,
+                                           int sig0, int sig1, int w) {
+    const teal_step_tp& T = *P.tp;
+    const int64_t off = (g.acc - T.acc[T.rank]) + (int64_t)tile * TW + threadIdx.x;
+    for (int j = 0; j < T.world; ++j) red_add_s64(T.acc[j] + off, fx);
+    __syncthreads();
+    if (threadIdx.x == 0 && sig0 >= 0) {
+        __threadfence_system();
+        for (int j = 0; j < T.world; ++j)
+            for (int c = sig0; c <= sig1; ++c) red_release_sys(T.counters[j] + (int64_t)c * CSTRIDE, w);
+    }
+}
+
 template <int WT, int UB>
 __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph, const teal_step_group& g, Smem& s,
                              uint64_t pol, unsigned long long* tl) {
@@ -750,7 +817,10 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
         wait_range(P.counters, g.xwait, g.xwait, g.xwait_target);
         rms_stage_x(g, s);
     }
-    if (ph.dep_kind == TEAL_DEP_GLOBAL) wait_range(P.counters, ph.dep, ph.dep, ph.target);
+    if (ph.dep_kind == TEAL_DEP_GLOBAL) {
+        if (P.tp) wait_range_sys(P.counters, ph.dep, ph.dep, ph.target);
+        else wait_range(P.counters, ph.dep, ph.dep, ph.target);
+    }
     // PRO_RMSNORM: rden computed by the first compaction, overlapped with its x loads
     float rden = rms ? -1.f : 1.f;
     if (racc) {
@@ -808,9 +878,13 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
         const int cl = owner_of((int64_t)(tile + 1) * gpt - 1, F, G);
         if (g.acc) {  // ACC output: add this CTA's partial, bump the counters by its share of CONTRIB
             if (g.col_scale) v *= g.col_scale[(int64_t)tile * TW + tid];
-            red_add_s64(g.acc + (int64_t)tile * TW + tid, to_fx(v));
-            signal(P.counters, tm.sig0, tm.sig1,
-                   g.ranges ? (segi == 0 ? rg.z : rg.w) : (c == cf ? CONTRIB - (cl - cf) : 1));
+            const int w = g.ranges ? (segi == 0 ? rg.z : rg.w) : (c == cf ? CONTRIB - (cl - cf) : 1);
+            if (g.tp_sum && P.tp) {
+                tp_accumulate(P, g, tile, to_fx(v), tm.sig0, tm.sig1, w);
+            } else {
+                red_add_s64(g.acc + (int64_t)tile * TW + tid, to_fx(v));
+                signal(P.counters, tm.sig0, tm.sig1, w);
+            }
             ++lasts;
             if (segi == 0) SL_STAMP(4, gtimer());
             continue;
@@ -1137,7 +1211,10 @@ __device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, S
     // the sequence length is written by this step's load phase: a CTA that had
     // no qkv slice reaches this point without having waited for it (the
     // phase's GLOBAL dependency; none when the load ran in an earlier launch)
-    if (ph.dep_kind == TEAL_DEP_GLOBAL) wait_range(P.counters, ph.dep, ph.dep, ph.target);
+    if (ph.dep_kind == TEAL_DEP_GLOBAL) {
+        if (P.tp) wait_range_sys(P.counters, ph.dep, ph.dep, ph.target);
+        else wait_range(P.counters, ph.dep, ph.dep, ph.target);
+    }
     const int L = __ldcg(P.state + 1);
     const int nact = min(a.nchunks, (L + a.chunk - 1) / a.chunk);  // chunks holding positions
     const int nu = a.KVH * nact;
@@ -1152,17 +1229,45 @@ __device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, S
     }
 }
 
+// Counter 0 (the step's load / accumulator zeroing) — with fused tensor
+// parallelism on every rank: no rank adds into a peer's accumulators before
+// that peer has zeroed them (targets world x grid).
+__device__ __forceinline__ void load_signal(const teal_step_plan& P) {
+    if (!P.tp) {
+        signal(P.counters, 0, 0);
+        return;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int j = 0; j < P.tp->world; ++j) red_release_sys(P.tp->counters[j], 1);
+    }
+}
+
 // ---- residual load: x = emb[token] (or x_in); ss partials; {pos, len} ---------
 __device__ __noinline__ void load_phase(const teal_step_plan& P) {
     Smem& s = smem();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (P.tp) {  // every rank has finished (and reset) the previous step before anyone signals this one
+        if (tid == 0) {
+            const unsigned* ep = P.tp->epoch[P.tp->rank];
+            const int mine = ld_acquire_sys(reinterpret_cast<const int*>(ep + P.tp->rank));
+            const unsigned long long t0 = gtimer_();
+            for (int j = 0; j < P.tp->world; ++j)
+                while (ld_acquire_sys(reinterpret_cast<const int*>(ep + j)) < mine) {
+                    __nanosleep(128);
+                    if (gtimer_() - t0 > 10000000000ull) asm volatile("trap;");
+                }
+        }
+        __syncthreads();
+    }
     if (P.acc_zero) {  // every CTA zeroes its share of this step's ACC accumulators (16 B stores)
         int4* z = reinterpret_cast<int4*>(P.acc_zero);
         const int64_t n2 = P.acc_zero_n >> 1;
         for (int64_t i = (int64_t)blockIdx.x * NT + tid; i < n2; i += (int64_t)gridDim.x * NT) z[i] = make_int4(0, 0, 0, 0);
     }
     if (blockIdx.x != 0) {
-        signal(P.counters, 0, 0);
+        load_signal(P);
         return;
     }
     if (tid == 0) {
@@ -1204,7 +1309,7 @@ __device__ __noinline__ void load_phase(const teal_step_plan& P) {
         }
         __syncthreads();
     }
-    signal(P.counters, 0, 0);
+    load_signal(P);
 }
 
 // ---- residual materialisation (plans without an LM head) --------------------
@@ -1235,12 +1340,20 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const __grid_constant__ 
         if (tl && tid == 0) tl[1] = gtimer();
     }
     if (tid == 0) {
-        __threadfence();
+        if (P.tp) __threadfence_system();
+        else __threadfence();
         const unsigned prev = atomicAdd(P.ctrl, 1u);
         if (prev == gridDim.x - 1u) {
             for (int i = 0; i < P.ncounters; ++i) P.counters[(int64_t)i * CSTRIDE] = 0;
             P.ctrl[0] = 0u;
             __threadfence();
+            if (P.tp) {  // this rank completed one more step: tell every rank
+                const teal_step_tp& T = *P.tp;
+                const unsigned e = T.epoch[T.rank][T.rank] + 1u;
+                __threadfence_system();
+                for (int j = 0; j < T.world; ++j)
+                    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(T.epoch[j] + T.rank), "r"(e) : "memory");
+            }
         }
     }
 }
@@ -1448,7 +1561,7 @@ int teal_step_launch(const teal_step_plan* p, cudaStream_t stream) {
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = p->noncoop ? 0 : 1;
     void* args[1] = {(void*)p};
     cudaLaunchKernelExC(&cfg, kernel_ptr(p->w_dtype), args);
     return check_launch("teal_step_launch");

@@ -50,7 +50,7 @@ class StepGroup(ctypes.Structure):
                 ("nq", c_i), ("nkv", c_i), ("head_dim", c_i), ("kv_dtype", c_i), ("w_dtype", c_i),
                 ("gscale", c_vp), ("group", c_i), ("t_all", c_f), ("tile_stride_b", c_i64), ("row_stride_b", c_i64),
                 ("acc", c_vp), ("in_acc", c_vp), ("x_out", c_vp), ("ranges", c_vp), ("nranges", c_i),
-                ("xsig", c_i), ("xwait", c_i), ("xwait_target", c_i), ("pad3_", c_i)]
+                ("xsig", c_i), ("xwait", c_i), ("xwait_target", c_i), ("tp_sum", c_i)]
 
 
 class StepAttn(ctypes.Structure):
@@ -70,7 +70,17 @@ class StepPlan(ctypes.Structure):
                 ("cand_v", c_vp), ("cand_i", c_vp), ("token_out", c_vp), ("lm_done", c_vp), ("timeline", c_vp),
                 ("nphases", c_i), ("ncounters", c_i), ("prefetch_bytes", c_i), ("pad_", c_i),
                 ("d", c_i), ("emb_dtype", c_i), ("w_dtype", c_i), ("ctas", c_i),
-                ("acc_zero", c_vp), ("acc_zero_n", c_i64), ("phase_begin", c_i), ("phase_end", c_i)]
+                ("acc_zero", c_vp), ("acc_zero_n", c_i64), ("tp", c_vp), ("noncoop", c_i), ("pad4_", c_i),
+                ("phase_begin", c_i), ("phase_end", c_i)]
+
+
+TP_MAX = 8
+
+
+class StepTP(ctypes.Structure):
+    _fields_ = [("acc", c_vp * TP_MAX), ("counters", c_vp * TP_MAX), ("epoch", c_vp * TP_MAX),
+                ("token", c_vp * TP_MAX), ("cand_v", c_vp), ("cand_i", c_vp), ("lm_ticket", c_vp),
+                ("world", c_i), ("rank", c_i), ("vocab_off", c_i), ("pad_", c_i)]
 
 
 PHASE_LOAD, PHASE_GEMV, PHASE_ATTN, PHASE_RESID = 0, 1, 2, 3

@@ -329,3 +329,94 @@ def run_lockstep_step(decs, from_token: bool = True, stream_h: int | None = None
             for o in ops:
                 o[1].copy_(vs)
                 o[3].copy_(is_)
+
+
+# ---- fused tensor parallelism: the exchange inside the persistent kernel --------
+class FusedTPGroup:
+    """Tensor parallelism with the exchange INSIDE the persistent step kernel:
+    one launch per rank per token, no collective calls.  Row-parallel o/down
+    contributors add their int64 fixed-point partials straight into every
+    rank's accumulator and bump every rank's tile counters (system-scope
+    release, `teal_step_tp`); consumers wait for world x CONTRIB per tile, so
+    the exchange overlaps the streaming tile by tile.  Step-start zeroing is a
+    cross-rank barrier (counter 0 signalled on every rank), a monotonic
+    per-rank epoch keeps a fast rank from signalling the next step before a
+    slow rank has reset its counters, and the vocabulary-parallel LM head
+    reduces its argmax candidates on rank 0 with one cross-rank ticket.
+
+    This class is the single-GPU validation harness of that protocol: every
+    rank's shard and buffers live on this device, the ranks' launches run
+    concurrently on separate streams (ordinary launches, each with 1/world of
+    the resident CTAs) and "peer memory" is the other ranks' buffers.  On a
+    multi-GPU box the same tables hold CUDA-IPC-mapped peer pointers."""
+
+    def __init__(self, shards, thresholds=None, **kw):
+        from . import engine as E
+        self.E = E
+        world = len(shards)
+        if not 1 <= world <= E.TP_MAX:
+            raise ValueError(f"1 <= world <= {E.TP_MAX}")
+        E._bind()
+        dev = RT.require_cuda()
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        code = RT.dtype_code(shards[0].layers[0].wqkv.dtype) if isinstance(shards[0], DecoderWeights) else None
+        per_sm = E.C.lib().teal_step_ctas_per_sm(code if code is not None else E.C.TEAL_BF16)
+        per = per_sm * sms // world
+        self.world = world
+        self.decs = [E.StepDecoder(sh, thresholds, ctas=per, **kw) for sh in shards]
+        d0 = self.decs[0]
+        self.vocab_local = d0.spec.vocab
+        nt_lm = d0.lm_t.ntiles if d0.spec.vocab else 0
+        self.cand_v = torch.zeros(max(1, world * nt_lm), device=dev)
+        self.cand_i = torch.zeros(max(1, world * nt_lm), device=dev, dtype=torch.int32)
+        self.lm_ticket = torch.zeros(1, device=dev, dtype=torch.int32)
+        self.epochs = [torch.zeros(world, device=dev, dtype=torch.int32) for _ in range(world)]
+        self._tp_dev = []
+        L = d0.spec.n_layers
+        for r, d in enumerate(self.decs):
+            T = E.StepTP()
+            for j, dj in enumerate(self.decs):
+                T.acc[j] = dj.acc.data_ptr()
+                T.counters[j] = dj.counters.data_ptr()
+                T.epoch[j] = self.epochs[j].data_ptr()
+                T.token[j] = dj.token.data_ptr()
+            T.cand_v, T.cand_i, T.lm_ticket = self.cand_v.data_ptr(), self.cand_i.data_ptr(), self.lm_ticket.data_ptr()
+            T.world, T.rank, T.vocab_off = world, r, r * self.vocab_local
+            t = torch.frombuffer(bytearray(bytes(T)), dtype=torch.uint8).to(dev)
+            self._tp_dev.append(t)
+            d.plan.tp, d.plan.noncoop = t.data_ptr(), 1
+            gr, ph = d._groups_host, d._phases_host
+            for l in range(L):  # row-parallel outputs: o, down
+                gr[4 * l + 1].tp_sum = 1
+                gr[4 * l + 3].tp_sum = 1
+            for p in range(len(ph)):  # global joins now count every rank's signals
+                if ph[p].dep_kind == E.DEP_GLOBAL:
+                    ph[p].target *= world
+            gr[2].xwait_target *= world  # gate/up of layer 0 stages x after counter 0
+            d._upload_plan()
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
+
+    def reset(self, start_pos: int = 0) -> None:
+        for d in self.decs:
+            d.reset(start_pos)
+        for e in self.epochs:
+            e.zero_()
+        self.lm_ticket.zero_()
+
+    @property
+    def token(self):
+        return self.decs[0].token
+
+    def set_token(self, tok: int) -> None:
+        for d in self.decs:
+            d.token.fill_(tok)
+
+    def step(self, from_token: bool = True) -> None:
+        """One decode step: every rank's launch, concurrently."""
+        cur = torch.cuda.current_stream()
+        for st in self.streams:
+            st.wait_stream(cur)
+        for d, st in zip(self.decs, self.streams):
+            d._launch(st.cuda_stream, from_token)
+        for st in self.streams:
+            cur.wait_stream(st)

@@ -257,3 +257,33 @@ def test_step_engine_tp_torch_distributed_world2():
             assert r[2][i] == int(ref.token.item())
             assert rel_err(r[1][i], ref.x.cpu().numpy()) < 1e-5
         assert np.array_equal(res[0][1][i], res[1][1][i])
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 4])
+def test_fused_tp_in_kernel_exchange(world):
+    # the exchange inside the kernel: ranks' launches run concurrently on one
+    # device and add into each other's accumulators / counters
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200 import engine as E
+    from paper_2408_14690_b200 import tp
+    from conftest import rel_err
+    spec = _tp_spec()
+    W = D.random_weights(spec, torch.bfloat16, seed=12)
+    thr = [[0.3, 0.4, 0.5, 0.02, 0.6, 0.7, 0.05]] * 2
+    ref = E.StepDecoder(W, thr, kv_dtype=torch.float32)
+    grp = tp.FusedTPGroup([tp.shard_weights(W, r, world) for r in range(world)], thr, kv_dtype=torch.float32)
+    ref.reset()
+    grp.reset()
+    for tok in [5, 17, 999, 3, 250, 7]:
+        ref.token.fill_(tok)
+        ref.step_token()
+        grp.set_token(tok)
+        grp.step()
+        torch.cuda.synchronize()
+        x0 = grp.decs[0].x.clone()
+        for d in grp.decs:
+            assert torch.equal(d.x, x0)
+            assert int(d.token.item()) == int(ref.token.item())
+        assert rel_err(x0.cpu().numpy(), ref.x.cpu().numpy()) < 1e-5
