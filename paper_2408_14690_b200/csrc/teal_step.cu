@@ -118,12 +118,15 @@ __device__ __forceinline__ void red_release_sys(int* p, int v) {
 // Counters signalled by other GPUs (fused tensor parallel): system-scope
 // acquire, and a watchdog — a wait that cannot complete (a peer that never
 // launched) traps after ~10 s instead of hanging the device.
-__device__ __noinline__ void wait_range_sys(const int* counters, int c0, int c1, int target) {
+__device__ __forceinline__ void wait_range_sys(const int* counters, int c0, int c1, int target) {
     if (threadIdx.x == 0) {
-        const unsigned long long t0 = gtimer_();
         for (int c = c0; c <= c1; ++c) {
+            if (ld_acquire_sys(counters + (int64_t)c * CSTRIDE) >= target) continue;
+            const unsigned long long t0 = gtimer_();
+            unsigned ns = 32;
             while (ld_acquire_sys(counters + (int64_t)c * CSTRIDE) < target) {
-                __nanosleep(128);
+                __nanosleep(ns);
+                ns = ns < 128 ? ns * 2 : 128;
                 if (gtimer_() - t0 > 10000000000ull) asm volatile("trap;");
             }
         }
@@ -776,8 +779,7 @@ __device__ __noinline__ void tp_accumulate(const teal_step_plan& P, const teal_s
     const int64_t off = (g.acc - T.acc[T.rank]) + (int64_t)tile * TW + threadIdx.x;
     for (int j = 0; j < T.world; ++j) red_add_s64(T.acc[j] + off, fx);
     __syncthreads();
-    if (threadIdx.x == 0 && sig0 >= 0) {
-        __threadfence_system();
+    if (threadIdx.x == 0 && sig0 >= 0) {  // (release: cumulative over the CTA's adds ordered by the barrier)
         for (int j = 0; j < T.world; ++j)
             for (int c = sig0; c <= sig1; ++c) red_release_sys(T.counters[j] + (int64_t)c * CSTRIDE, w);
     }
@@ -1238,10 +1240,8 @@ __device__ __forceinline__ void load_signal(const teal_step_plan& P) {
         return;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
+    if (threadIdx.x == 0)
         for (int j = 0; j < P.tp->world; ++j) red_release_sys(P.tp->counters[j], 1);
-    }
 }
 
 // ---- residual load: x = emb[token] (or x_in); ss partials; {pos, len} ---------
