@@ -78,6 +78,9 @@ def parse():
                     help="config 4: tensor-parallel decode over the N ranks (persistent step kernel per rank, "
                          "NCCL int64 all-reduce of the row-parallel accumulators) instead of N replicas")
     ap.add_argument("--tp-model", choices=["8b", "70b"], default="70b")
+    ap.add_argument("--fused", action="store_true",
+                    help="with --tp: the exchange inside the kernel (peer memory over CUDA IPC / NVLink), "
+                         "one launch per token per GPU, no collective calls")
     return ap.parse_args()
 
 
@@ -533,16 +536,25 @@ def run_tp(args):
         import torch.distributed as dist
         dist.broadcast(thr_t, 0)
     thr = thr_t.cpu().tolist()
-    dec = tp.TPStepDecoder(W, thr, rank=rank, world=ws, full_vocab=spec.vocab, count_kept=True)
+    if args.fused:
+        dec = tp.FusedTPRank(W, thr, rank=rank, world=ws, count_kept=True)
+        step = dec.step
+    else:
+        dec = tp.TPStepDecoder(W, thr, rank=rank, world=ws, full_vocab=spec.vocab, count_kept=True)
 
-    def step():
-        if ws > 1:
-            tp.run_step_dist_step(dec)
-        else:
-            tp.run_lockstep_step([dec])
+        def step():
+            if ws > 1:
+                tp.run_step_dist_step(dec)
+            else:
+                tp.run_lockstep_step([dec])
 
-    dec.reset()
-    dec.token.fill_(1)
+    def reset():
+        dec.reset()
+        dec.token.fill_(1)
+        torch.cuda.synchronize()
+        barrier(ws)
+
+    reset()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -562,8 +574,7 @@ def run_tp(args):
     except Exception as e:  # keep the eager path (reported in config)
         print(f"[bench --tp] graph capture failed ({e}); timing eager steps", file=sys.stderr)
         graphed = False
-    dec.reset()
-    dec.token.fill_(1)
+    reset()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -593,7 +604,8 @@ def run_tp(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"llama3-{args.tp_model} random-init batch-1 decode, tensor parallel",
                        "sparsity": args.sparsity, "batch": 1, "parallelism": f"tp{ws}",
-                       "collective": "NCCL int64 all-reduce of row-parallel accumulators" if ws > 1 else "none",
+                       "collective": ("in-kernel peer-memory accumulate (CUDA IPC / NVLink)" if args.fused else
+                                      "NCCL int64 all-reduce of row-parallel accumulators") if ws > 1 else "none",
                        "cuda_graph": graphed,
                        "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "kernel": "teal step_kernel per rank (algorithmic bytes of rank 0 / step time)",
@@ -602,7 +614,7 @@ def run_tp(args):
             "cpu_baseline": None,
             "e2e": {"value": round(args.steps * 1e3 / ms_e2e, 2), "unit": UNIT, "h2d_bytes_per_step": 4,
                     "d2h_bytes_per_step": 4},
-            "gpu_launches": (2 * spec.n_layers + 1) * args.steps,
+            "gpu_launches": (1 if args.fused else 2 * spec.n_layers + 1) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

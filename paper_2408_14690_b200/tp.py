@@ -332,6 +332,34 @@ def run_lockstep_step(decs, from_token: bool = True, stream_h: int | None = None
 
 
 # ---- fused tensor parallelism: the exchange inside the persistent kernel --------
+def _attach_tp(d, peers, cand_v, cand_i, lm_ticket, rank: int, world: int, vocab_off: int, noncoop: bool):
+    """Point rank `rank`'s StepDecoder `d` at its TP group: the teal_step_tp
+    table (every rank's accumulator / counters / epoch / token pointers, the
+    LM candidates and ticket on rank 0), row-parallel o/down outputs summed
+    into every rank, and every global join counting world ranks' signals."""
+    from . import engine as E
+    T = E.StepTP()
+    for j, pj in enumerate(peers):
+        T.acc[j] = pj["acc"].data_ptr()
+        T.counters[j] = pj["counters"].data_ptr()
+        T.epoch[j] = pj["epoch"].data_ptr()
+        T.token[j] = pj["token"].data_ptr()
+    T.cand_v, T.cand_i, T.lm_ticket = cand_v.data_ptr(), cand_i.data_ptr(), lm_ticket.data_ptr()
+    T.world, T.rank, T.vocab_off = world, rank, vocab_off
+    t = torch.frombuffer(bytearray(bytes(T)), dtype=torch.uint8).to(d.device)
+    d.plan.tp, d.plan.noncoop = t.data_ptr(), int(noncoop)
+    gr, ph = d._groups_host, d._phases_host
+    for l in range(d.spec.n_layers):  # row-parallel outputs: o, down
+        gr[4 * l + 1].tp_sum = 1
+        gr[4 * l + 3].tp_sum = 1
+    for p in range(len(ph)):  # global joins now count every rank's signals
+        if ph[p].dep_kind == E.DEP_GLOBAL:
+            ph[p].target *= world
+    gr[2].xwait_target *= world  # gate/up of layer 0 stages x after counter 0
+    d._upload_plan()
+    return t
+
+
 class FusedTPGroup:
     """Tensor parallelism with the exchange INSIDE the persistent step kernel:
     one launch per rank per token, no collective calls.  Row-parallel o/down
@@ -372,28 +400,11 @@ class FusedTPGroup:
         self.lm_ticket = torch.zeros(1, device=dev, dtype=torch.int32)
         self.epochs = [torch.zeros(world, device=dev, dtype=torch.int32) for _ in range(world)]
         self._tp_dev = []
-        L = d0.spec.n_layers
         for r, d in enumerate(self.decs):
-            T = E.StepTP()
-            for j, dj in enumerate(self.decs):
-                T.acc[j] = dj.acc.data_ptr()
-                T.counters[j] = dj.counters.data_ptr()
-                T.epoch[j] = self.epochs[j].data_ptr()
-                T.token[j] = dj.token.data_ptr()
-            T.cand_v, T.cand_i, T.lm_ticket = self.cand_v.data_ptr(), self.cand_i.data_ptr(), self.lm_ticket.data_ptr()
-            T.world, T.rank, T.vocab_off = world, r, r * self.vocab_local
-            t = torch.frombuffer(bytearray(bytes(T)), dtype=torch.uint8).to(dev)
-            self._tp_dev.append(t)
-            d.plan.tp, d.plan.noncoop = t.data_ptr(), 1
-            gr, ph = d._groups_host, d._phases_host
-            for l in range(L):  # row-parallel outputs: o, down
-                gr[4 * l + 1].tp_sum = 1
-                gr[4 * l + 3].tp_sum = 1
-            for p in range(len(ph)):  # global joins now count every rank's signals
-                if ph[p].dep_kind == E.DEP_GLOBAL:
-                    ph[p].target *= world
-            gr[2].xwait_target *= world  # gate/up of layer 0 stages x after counter 0
-            d._upload_plan()
+            peers = [dict(acc=dj.acc, counters=dj.counters, epoch=self.epochs[j], token=dj.token)
+                     for j, dj in enumerate(self.decs)]
+            self._tp_dev.append(_attach_tp(d, peers, self.cand_v, self.cand_i, self.lm_ticket, r, world,
+                                           r * self.vocab_local, noncoop=True))
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
 
     def reset(self, start_pos: int = 0) -> None:
@@ -420,3 +431,55 @@ class FusedTPGroup:
             d._launch(st.cuda_stream, from_token)
         for st in self.streams:
             cur.wait_stream(st)
+
+
+class FusedTPRank:
+    """One rank (one process, one GPU) of fused tensor parallelism: the same
+    in-kernel exchange as :class:`FusedTPGroup`, with the peers' accumulator,
+    counter, epoch and token buffers mapped into this process over CUDA IPC
+    (torch's tensor IPC; NVLink peer access) once at setup.  Every rank then
+    launches its own cooperative step kernel per token — no collective calls
+    on the data path.  (On this single-GPU development box only world 1 runs:
+    two processes on one GPU time-slice, so their kernels cannot wait for each
+    other; the protocol itself is validated by FusedTPGroup.)"""
+
+    def __init__(self, shard, thresholds=None, rank: int = 0, world: int = 1, group=None, **kw):
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        from . import engine as E
+        self.rank, self.world = rank, world
+        self.dec = d = E.StepDecoder(shard, thresholds, **kw)
+        dev = d.device
+        self.epoch = torch.zeros(world, device=dev, dtype=torch.int32)
+        nt_lm = d.lm_t.ntiles if d.spec.vocab else 0
+        mine = dict(acc=d.acc, counters=d.counters, epoch=self.epoch, token=d.token)
+        if rank == 0:
+            mine.update(cand_v=torch.zeros(max(1, world * nt_lm), device=dev),
+                        cand_i=torch.zeros(max(1, world * nt_lm), device=dev, dtype=torch.int32),
+                        lm_ticket=torch.zeros(1, device=dev, dtype=torch.int32))
+        self._mine = mine
+        if world > 1:
+            shared = {k: reduce_tensor(v) for k, v in mine.items()}
+            allh = [None] * world
+            dist.all_gather_object(allh, shared, group=group)
+            peers = [mine if j == rank else {k: fn(*args) for k, (fn, args) in h.items()} for j, h in enumerate(allh)]
+        else:
+            peers = [mine]
+        self._peers = peers  # keep the mappings alive
+        self._tp_dev = _attach_tp(d, peers, peers[0]["cand_v"], peers[0]["cand_i"], peers[0]["lm_ticket"],
+                                  rank, world, rank * d.spec.vocab, noncoop=False)
+        self.token = d.token
+
+    def reset(self, start_pos: int = 0) -> None:
+        """Call on every rank (then synchronise) before the first step."""
+        self.dec.reset(start_pos)
+        self.epoch.zero_()
+        if self.rank == 0:
+            self._mine["lm_ticket"].zero_()
+
+    @property
+    def x(self):
+        return self.dec.x
+
+    def step(self) -> None:
+        self.dec.step_token()

@@ -287,3 +287,27 @@ def test_fused_tp_in_kernel_exchange(world):
             assert torch.equal(d.x, x0)
             assert int(d.token.item()) == int(ref.token.item())
         assert rel_err(x0.cpu().numpy(), ref.x.cpu().numpy()) < 1e-5
+
+
+@pytest.mark.gpu
+def test_fused_tp_rank_world1_runs_the_rank_path():
+    # FusedTPRank's plumbing (tp table, cooperative launch, epochs, LM ticket
+    # on "rank 0") at world 1 against the plain engine
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200 import engine as E
+    from paper_2408_14690_b200 import tp
+    spec = _tp_spec()
+    W = D.random_weights(spec, torch.bfloat16, seed=12)
+    thr = [[0.3, 0.4, 0.5, 0.02, 0.6, 0.7, 0.05]] * 2
+    ref = E.StepDecoder(W, thr, kv_dtype=torch.float32)
+    r0 = tp.FusedTPRank(W, thr, rank=0, world=1, kv_dtype=torch.float32)
+    ref.reset()
+    r0.reset()
+    for tok in [5, 17, 999, 3]:
+        ref.token.fill_(tok)
+        ref.step_token()
+        r0.token.fill_(tok)
+        r0.step()
+        torch.cuda.synchronize()
+        assert int(r0.token.item()) == int(ref.token.item())
+        assert torch.equal(r0.x, ref.x)
