@@ -85,8 +85,6 @@ class StepTP(ctypes.Structure):
 
 PHASE_LOAD, PHASE_GEMV, PHASE_ATTN, PHASE_RESID = 0, 1, 2, 3
 PRO_RMS_ACC, PRO_SILU_ACC = 2, 3
-import os as _os
-_NO_QKV_ACC = _os.environ.get("TEAL_NO_QKV_ACC") == "1"
 CONTRIB = 1024  # TEAL_STEP_CONTRIB: counter units per finished tile of an ACC output
 XS_MAX = 8192   # PRO_RMS_ACC staging limit on d
 DEP_NONE, DEP_GLOBAL, DEP_ROWS = 0, 1, 2
@@ -533,20 +531,20 @@ class StepDecoder:
                     feeds[gg] += 1
                 meta.append(StepTile(_t32(t[sl]), _t32(t[sh]), sl, sh, fl, fh, cb["attn"] + g0, cb["attn"] + g1))
             groups.append(self._group(tw["qkv"], tiles_tensor(meta), m=d, n=nq + 2 * nkv, maxc=mc["qkv"],
-                                      gain=lw.rms_attn, ws="qkv", **qkv_in, acc=None if _NO_QKV_ACC else A["qkv"],
+                                      gain=lw.rms_attn, ws="qkv", **qkv_in, acc=A["qkv"],
                                       epilogue=SEPI_QKV, q_out=self.q, k_cache=kc, v_cache=vc,
                                       dbg=(T.h["pre_attn"][l] if T else None,
                                            [T.bits[p][l] for p in ("q", "k", "v")] if T else None,
                                            [K[l, PROJ.index(p)] for p in ("q", "k", "v")] if K is not None else None)))
             phases.append(StepPhase(PHASE_GEMV, len(groups) - 1, DEP_GLOBAL, dep_in[0], dep_in[1], 1))
             # --- attention per (kv group, position chunk)
-            tgt = torch.tensor([f_ * (1 if _NO_QKV_ACC else K_) for f_ in feeds], dtype=torch.int32, device=dev)
+            tgt = torch.tensor([f_ * K_ for f_ in feeds], dtype=torch.int32, device=dev)
             keep.append(tgt)
             attns.append(StepAttn(self.q.data_ptr(), kc.data_ptr(), vc.data_ptr(), self.ctx.data_ptr(),
                                   self.ws["attn"].data_ptr(), self.tk["attn"].data_ptr(), spec.max_seq,
                                   spec.n_heads, KVH, hd, RT.dtype_code(self.kv_dtype), self.attn_chunk,
                                   self.nchunks, cb["odep"], cb["attn"], tgt.data_ptr(), RT.ptr(self.attn_dbg),
-                                  None if _NO_QKV_ACC else A["qkv"].data_ptr(), RT.ptr(self.rope_cos), RT.ptr(self.rope_sin), nq, nkv))
+                                  A["qkv"].data_ptr(), RT.ptr(self.rope_cos), RT.ptr(self.rope_sin), nq, nkv))
             phases.append(StepPhase(PHASE_ATTN, len(attns) - 1, DEP_GLOBAL, 0, Gc, 1))  # step state from the load
             # --- o: rows = context channels, each waits for its kv group's context
             tv = _t32(t[3])

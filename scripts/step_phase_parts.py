@@ -1,8 +1,10 @@
 """Median-CTA composition of each GEMV phase of the persistent step (layers
-1-5 of an 8-layer Llama-3-8B-shaped model at s=0.5, 10 steps): poll = wait
-for the global dependency, prep = prologue (RMS finish / row deps),
-stream1 = compaction + streaming of the first segment, tail = reduction and
-signals; end_spread = latest minus median CTA end."""
+1-5 of an 8-layer Llama-3-8B-shaped model at s=0.5, 10 steps): ready = from the
+CTA's phase start to its first segment's rows being ready (dependency wait +
+RMS prologue / row dependencies), stream1 = compaction + streaming of the
+first segment, tail = reduction and signals; end_spread = latest minus
+median CTA end; start_to_prevmax = how long before the previous phase's
+last CTA the median CTA entered this phase."""
 import sys
 from pathlib import Path
 import torch
@@ -27,11 +29,10 @@ for _ in range(10):
         nm = names[p]
         if nm == "attn": continue
         ok = t[:, p, 2] > 0
-        st = t[ok, p, 0]; dep = t[ok, p, 7]; s2 = t[ok, p, 2]; s3 = t[ok, p, 3]; en = t[ok, p, 1]
+        st = t[ok, p, 0]; s2 = t[ok, p, 2]; s3 = t[ok, p, 3]; en = t[ok, p, 1]
         prev_end_max = t[:, p - 1, 1].max()
-        d = acc.setdefault(nm, {k: [] for k in ("poll", "prep", "stream1", "tail", "end_spread", "start_to_prevmax")})
-        d["poll"].append(float((dep - st).median()) / 1e3)
-        d["prep"].append(float((s2 - dep).median()) / 1e3)
+        d = acc.setdefault(nm, {k: [] for k in ("ready", "stream1", "tail", "end_spread", "start_to_prevmax")})
+        d["ready"].append(float((s2 - st).median()) / 1e3)
         d["stream1"].append(float((s3 - s2).median()) / 1e3)
         d["tail"].append(float((en - s3).median()) / 1e3)
         d["end_spread"].append(float(en.max() - en.median()) / 1e3)
