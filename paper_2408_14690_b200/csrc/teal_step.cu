@@ -562,17 +562,18 @@ __device__ int compact_rows(const teal_step_group& g, const teal_step_tile& tm, 
     const bool two = tm.seg_hi != tm.seg_lo;
     constexpr int RPT = MAXR / NT;  // rows per thread
     float hx[RPT], gx[RPT];
+    // Loads are straight-line (rows past r1 read row r0 and are ignored by
+    // the compaction): a branch per row would make the compiler wait on each
+    // load at the reconvergence point instead of keeping them all in flight.
     if (g.prologue == TEAL_PRO_SILU_ACC) {  // h = silu(gate) * up from the gate/up accumulator
         long long ga[RPT], ua[RPT];
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
             const int i = r0 + q * NT + tid;
-            ga[q] = ua[q] = 0;
-            if (i < r1) {
-                const int64_t b = (int64_t)(i / TH) * TW + (i % TH);
-                ga[q] = __ldcg(g.in_acc + b);
-                ua[q] = __ldcg(g.in_acc + b + TH);
-            }
+            const int ic = i < r1 ? i : r0;
+            const int64_t b = (int64_t)(ic / TH) * TW + (ic % TH);
+            ga[q] = __ldcg(g.in_acc + b);
+            ua[q] = __ldcg(g.in_acc + b + TH);
         }
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
@@ -580,15 +581,23 @@ __device__ int compact_rows(const teal_step_group& g, const teal_step_tile& tm, 
             gx[q] = 1.f;
         }
     } else {
+        if (g.prologue == TEAL_PRO_RMS_ACC) {
 #pragma unroll
-        for (int q = 0; q < RPT; ++q) {  // all x (and gain) loads in flight at once
-            const int i = r0 + q * NT + tid;
-            hx[q] = 0.f;
-            gx[q] = 1.f;
-            if (i < r1) {
-                hx[q] = g.prologue == TEAL_PRO_RMS_ACC ? s.u.g.xs[i] : __ldcg(g.x + i);
-                if (rms) gx[q] = __ldg(g.gain + i);
+            for (int q = 0; q < RPT; ++q) {
+                const int i = r0 + q * NT + tid;
+                hx[q] = s.u.g.xs[i < r1 ? i : r0];
             }
+        } else {
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {  // all x loads in flight at once
+                const int i = r0 + q * NT + tid;
+                hx[q] = __ldcg(g.x + (i < r1 ? i : r0));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const int i = r0 + q * NT + tid;
+            gx[q] = rms ? __ldg(g.gain + (i < r1 ? i : r0)) : 1.f;
         }
     }
     if (rms) {
