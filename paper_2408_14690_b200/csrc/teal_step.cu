@@ -487,7 +487,7 @@ __device__ void rms_stage_x(const teal_step_group& g, Smem& s) {
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
             const int i = i0 + q * NT + tid;
-            xb[q] = i < m ? __ldcg(g.x + i) : 0.f;
+            xb[q] = __ldcg(g.x + (i < m ? i : 0));  // straight-line (unused past m)
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
@@ -507,7 +507,7 @@ __device__ float rms_acc_finish(const teal_step_group& g, int c, int G, Smem& s)
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
             const int i = i0 + q * NT + tid;
-            xa[q] = i < m ? __ldcg(g.in_acc + i) : 0;
+            xa[q] = __ldcg(g.in_acc + (i < m ? i : 0));
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
@@ -968,9 +968,11 @@ __device__ __noinline__ void attn_stage_kv(const teal_step_attn& a, int p0, int 
     const uint4* gv = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(a.v_cache) + (kvbase + (int64_t)p0 * hd) * kvb);
     uint4 kk[PER], vv[PER];
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
+    for (int q = 0; q < PER; ++q) {  // straight-line: out-of-range vectors re-read vector 0 (unused)
         const int v = tid + q * NT;
-        if (v < n16 && v / vpr != newrow) { kk[q] = __ldcg(gk + v); vv[q] = __ldcg(gv + v); }
+        const int vc = v < n16 ? v : 0;
+        kk[q] = __ldcg(gk + vc);
+        vv[q] = __ldcg(gv + vc);
     }
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
@@ -999,27 +1001,28 @@ __device__ __noinline__ void attn_stage_q(const teal_step_attn& a, int g, int po
         cs = __ldg(a.rope_cos + (int64_t)pos * half + dd);
         sn = __ldg(a.rope_sin + (int64_t)pos * half + dd);
     }
-#pragma unroll
-    for (int j = 0; j < QPT; ++j) {
-        const int o = tid + j * NT;
-        const int64_t qc = (int64_t)g * G * hd + o;
-        qa[j] = qp[j] = 0;
-        qf[j] = 0.f;
-        if (o < G * hd) {
-            if (!acc) {
-                qf[j] = __ldcg(a.q + qc);
-            } else {
-                qa[j] = __ldcg(a.qkv_acc + qc);
-                if (rope) qp[j] = __ldcg(a.qkv_acc + qc + part);
-            }
-        }
-    }
+    // straight-line loads (clamped indices; unused values are never consumed)
     const bool nk = newrow >= 0 && tid < hd;
-    const int64_t kc = (int64_t)a.nq + (int64_t)g * hd + tid;
-    if (nk) {
+    if (acc) {
+#pragma unroll
+        for (int j = 0; j < QPT; ++j) {
+            const int o = tid + j * NT;
+            const int64_t qc = (int64_t)g * G * hd + (o < G * hd ? o : d);
+            qa[j] = __ldcg(a.qkv_acc + qc);
+            qp[j] = __ldcg(a.qkv_acc + qc + part);
+            qf[j] = 0.f;
+        }
+        const int64_t kc = (int64_t)a.nq + (int64_t)g * hd + d;
         ka = __ldcg(a.qkv_acc + kc);
-        if (rope) kp = __ldcg(a.qkv_acc + kc + part);
+        kp = __ldcg(a.qkv_acc + kc + part);
         va = __ldcg(a.qkv_acc + kc + a.nkv);
+    } else {
+#pragma unroll
+        for (int j = 0; j < QPT; ++j) {
+            const int o = tid + j * NT;
+            qf[j] = __ldcg(a.q + (int64_t)g * G * hd + (o < G * hd ? o : 0));
+            qa[j] = qp[j] = 0;
+        }
     }
     const float sgn = d < half ? -1.f : 1.f;  // x*cos -/+ partner*sin
 #pragma unroll
