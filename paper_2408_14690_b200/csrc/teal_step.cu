@@ -1378,9 +1378,10 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const __grid_constant__ 
     }
 }
 
-// Kernel variant: default 2 CTAs/SM with 8 rows per pipeline stage (128
-// registers, no spills in the streaming loop); TEAL_STEP_OCC=3 selects 3
-// CTAs/SM with 4 rows per stage (80 registers; measured slower: spills).
+// Kernel variant: default 2 CTAs/SM with 6 rows per pipeline stage (128
+// registers; measured on the 8B step: UB 5 / 6 / 7 / 8 / 10 -> 370 / 413 /
+// 410 / 406 / 361 tok/s at 50%); TEAL_STEP_OCC=3 selects 3 CTAs/SM with 4
+// rows per stage (80 registers; measured slower: spills).
 static int occ_mode() {
     static int v = -1;
     if (v < 0) {
@@ -1392,7 +1393,7 @@ static int occ_mode() {
 
 template <int WT>
 static void* kernel_ptr_t() {
-    if (occ_mode() == 2) return (void*)step_kernel<WT, 2, 8>;
+    if (occ_mode() == 2) return (void*)step_kernel<WT, 2, 6>;
     return (void*)step_kernel<WT, 3, 4>;
 }
 
