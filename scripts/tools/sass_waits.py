@@ -9,7 +9,7 @@ import subprocess
 import sys
 
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_2408_14690_b200/lib/libteal_b200.so"
-fn = sys.argv[2] if len(sys.argv) > 2 else "step_kernelILi1ELi2ELi8E"
+fn = sys.argv[2] if len(sys.argv) > 2 else "step_kernelILi1ELi2ELi6E"
 out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
 lines = out.split("\n")
 ins = []
