@@ -870,12 +870,22 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
         for (int j = 0; j < 8; ++j) acc[j] = 0.f;
         for (int ra = r0; ra < r1; ra += MAXR) {
             const int rb = min(r1, ra + MAXR);
-            const int cnt = compact_rows(g, tm, tile, ra, rb, rden, rms, s);
-            if constexpr (WT == TEAL_I4) {  // stage the chunk's row-group scales (one L2 round trip)
-                const int gA = ra / g.group, gB = (rb - 1) / g.group;
-                for (int q = tid; q < (gB - gA + 1) * TW; q += NT)
-                    s.u.g.gsc[q] = __ldg(g.gscale + (int64_t)(gA + q / TW) * g.ntiles * TW + (int64_t)tile * TW + q % TW);
+            int cnt;
+            if constexpr (WT == TEAL_I4) {
+                // the chunk's row-group scales: every load in flight together and
+                // under the compaction (thread = column; one round trip, hidden)
+                const int gA = ra / g.group, ng = (rb - 1) / g.group - gA + 1;
+                float sc[GSC_MAX];
+#pragma unroll
+                for (int k = 0; k < GSC_MAX; ++k)
+                    sc[k] = __ldg(g.gscale + (int64_t)(gA + (k < ng ? k : 0)) * g.ntiles * TW + (int64_t)tile * TW + tid);
+                cnt = compact_rows(g, tm, tile, ra, rb, rden, rms, s);
+#pragma unroll
+                for (int k = 0; k < GSC_MAX; ++k)
+                    if (k < ng) s.u.g.gsc[k * TW + tid] = sc[k];
                 __syncthreads();
+            } else {
+                cnt = compact_rows(g, tm, tile, ra, rb, rden, rms, s);
             }
             stream_rows<WT, UB>(tbase + (int64_t)ra * rsb, rsb, cnt, s, acc, pol, ra, g.group > 0 ? g.group : 1,
                                 ok_lo, ok_hi);
