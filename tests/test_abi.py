@@ -103,3 +103,23 @@ def test_rng_stream_reproduces_reference_draws():
     b = R.philox_generator(202, 0).standard_normal(1000, dtype=np.float32)
     assert a.tobytes() == b.tobytes()
     assert T.RngStream(5).child(1).seed == R.child_seed(5, 1)
+
+
+def test_cli_bench_parser_and_errors():
+    # the reference CLI's bench flags parse; invalid arguments exit 2 before any GPU work
+    from paper_2408_14690_b200 import cli
+    a = cli.build_parser().parse_args(["bench", "--rows", "64", "--cols", "96", "--sparsities", "0,0.5"])
+    assert (a.rows, a.cols, a.reps, a.warmup, a.dtype) == (64, 96, 100, 10, "f32")
+    assert cli.main(["bench", "--sparsities", "0,x"]) == cli.EXIT_INVALID
+    assert cli._fmt_cell(0.1 + 0.2) == "0.3" and cli._fmt_cell(7) == "7"
+
+
+@pytest.mark.gpu
+def test_cli_bench_tsv(tmp_path):
+    from paper_2408_14690_b200 import cli
+    out = tmp_path / "bench.tsv"
+    assert cli.main(["bench", "--rows", "256", "--cols", "512", "--sparsities", "0,0.5", "--reps", "10",
+                     "--warmup", "3", "--out", str(out)]) == cli.EXIT_OK
+    lines = out.read_text().splitlines()
+    assert lines[0].split("\t") == ["sparsity", "median_ns", "min_ns", "dense_median_ns", "speedup", "weight_bytes"]
+    assert len(lines) == 3 and (tmp_path / "bench.tsv.manifest.json").exists()
