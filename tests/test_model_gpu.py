@@ -257,3 +257,23 @@ class TestGreedyGPU:
         for n in T.MATRIX_NAMES:
             expected.extend([n] * int(np.ceil(1.0 / (policy.alpha * total / fp[n]))))
         assert [s.chosen for s in trace.steps[1:]] == expected
+
+
+@pytest.mark.gpu
+def test_sparse_prefill_dense_prefix(toy_model):
+    # TEAL's prefill: positions before `dense_prefix` stay dense (attention
+    # sinks).  Causality makes those rows identical to the dense forward; the
+    # prefix 0 / full-length ends reproduce the sparse / dense forwards.
+    g = golden("toy_model")
+    thr = [g[f"thr50_{b}"].tolist() for b in range(2)]
+    cfgs = [T.BlockSparsityConfig({n: 0.5 for n in T.MATRIX_NAMES}, dict(zip(T.MATRIX_NAMES, t))) for t in thr]
+    X = torch.from_numpy(g["X"][:32]).cuda()
+    dense = T.model_forward_dense(toy_model, X)
+    sparse = T.model_forward_sparse(toy_model, X, cfgs)
+    assert torch.equal(T.model_forward_sparse(toy_model, X, cfgs, dense_prefix=0), sparse)
+    assert torch.equal(T.model_forward_sparse(toy_model, X, cfgs, dense_prefix=32), dense)
+    mixed = T.model_forward_sparse(toy_model, X, cfgs, dense_prefix=12)
+    assert torch.equal(mixed[:12], dense[:12])
+    assert not torch.equal(mixed[12:], dense[12:]) and not torch.equal(mixed[12:], sparse[12:])
+    with pytest.raises(ValueError, match="dense_prefix"):
+        T.model_forward_sparse(toy_model, X, cfgs, dense_prefix=-1)
