@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_kernel(const __grid_consta
     constexpr int LB = RowLoad<WT, CPL>::BYTES;
     constexpr int U = 4;
     __shared__ int s_idx[CHUNK];
-    __shared__ float s_x[CHUNK * BM];
+    __shared__ __align__(16) float s_x[CHUNK * BM];
     __shared__ float s_red[BM * TC];
     __shared__ int s_wcnt[NW];
     __shared__ int s_last;
@@ -129,9 +129,14 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_kernel(const __grid_consta
             const bool v = i < rb;
             float xs[BM];
             float s = 0.f;
+            // straight-line loads (clamped indices, masked after): a load
+            // inside a per-element branch is waited for at the branch's
+            // reconvergence point, i.e. B round trips instead of one
+#pragma unroll
+            for (int b = 0; b < BM; ++b) xs[b] = __ldg(A.x + (int64_t)(b < B ? b : 0) * A.m + (v ? i : ra));
 #pragma unroll
             for (int b = 0; b < BM; ++b) {
-                xs[b] = (v && b < B) ? A.x[(int64_t)b * A.m + i] : 0.f;
+                xs[b] = (v && b < B) ? xs[b] : 0.f;
                 if (b < B) s = __fadd_rn(s, fabsf(xs[b]));
             }
             const float mean = (float)__ddiv_rn((double)s, (double)B);
@@ -157,10 +162,10 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_kernel(const __grid_consta
                 for (int b = 0; b < BM; ++b) s_x[pos * BM + b] = xs[b];
             }
             __syncthreads();
-            // stream the kept rows: warp w takes entries w*U.., U rows in flight
-            for (int e0 = warp * U; e0 < tot; e0 += NW * U) {
-                uint4 d[U];
-                int rows[U];
+            // stream the kept rows: warp w takes entries w*U.., the next U
+            // rows' loads issued before the current U are consumed (double
+            // buffer: 2U row chunks in flight per warp)
+            auto fetch = [&](int e0, uint4 (&d)[U], int (&rows)[U]) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int e = e0 + u;
@@ -173,6 +178,8 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_kernel(const __grid_consta
                         d[u] = ld_row<LB>(p);
                     }
                 }
+            };
+            auto consume = [&](int e0, const uint4 (&d)[U], const int (&rows)[U]) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     if (rows[u] < 0) continue;
@@ -190,11 +197,40 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_kernel(const __grid_consta
                         for (int k = 0; k < CPL; ++k) w[k] *= sc[k];
                     }
                     const float* xr = s_x + (e0 + u) * BM;
+                    float xv[BM];
+                    if constexpr (BM % 4 == 0) {  // 16-byte shared loads of the batch's x values
+#pragma unroll
+                        for (int b = 0; b < BM; b += 4) {
+                            const float4 q = *reinterpret_cast<const float4*>(xr + b);
+                            xv[b] = q.x; xv[b + 1] = q.y; xv[b + 2] = q.z; xv[b + 3] = q.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < BM; ++b) xv[b] = xr[b];
+                    }
 #pragma unroll
                     for (int b = 0; b < BM; ++b) {
-                        const float xb = xr[b];
 #pragma unroll
-                        for (int k = 0; k < CPL; ++k) acc[b][k] = fmaf(xb, w[k], acc[b][k]);
+                        for (int k = 0; k < CPL; ++k) acc[b][k] = fmaf(xv[b], w[k], acc[b][k]);
+                    }
+                }
+            };
+            {
+                uint4 da[U], db[U];
+                int ra_[U], rb_[U];
+                int e0 = warp * U;
+                if (e0 < tot) {
+                    fetch(e0, da, ra_);
+                    for (;;) {
+                        const int en = e0 + NW * U;
+                        if (en < tot) fetch(en, db, rb_);
+                        consume(e0, da, ra_);
+                        if (en >= tot) break;
+                        e0 = en;
+                        if (e0 + NW * U < tot) fetch(e0 + NW * U, da, ra_);
+                        consume(e0, db, rb_);
+                        if (e0 + NW * U >= tot) break;
+                        e0 += NW * U;
                     }
                 }
             }
@@ -233,10 +269,22 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_kernel(const __grid_consta
             __syncthreads();
             fin = s_last != 0;
             if (fin) {
+                // every contributor's partial of this thread's outputs in flight
+                // together (16 at a time, clamped indices), then summed in
+                // ascending contributor order
                 const float* base = A.ws + (int64_t)tile * P.maxc * (BM * TC);
+                const int nc = cl - cf + 1;
                 for (int q = tid; q < BM * TC; q += NT) {
                     float v = 0.f;
-                    for (int k = 0; k <= cl - cf; ++k) v += __ldcg(base + (int64_t)k * (BM * TC) + q);
+                    for (int k0 = 0; k0 < nc; k0 += 16) {
+                        float pv[16];
+#pragma unroll
+                        for (int k = 0; k < 16; ++k)
+                            pv[k] = __ldcg(base + (int64_t)(k0 + k < nc ? k0 + k : 0) * (BM * TC) + q);
+#pragma unroll
+                        for (int k = 0; k < 16; ++k)
+                            if (k0 + k < nc) v += pv[k];
+                    }
                     s_red[q] = v;
                 }
                 __syncthreads();
