@@ -350,6 +350,9 @@ typedef struct teal_step_attn {
     const float* rope_cos;   /* nullable [max_seq][hd/2]                      */
     const float* rope_sin;
     int nq, nkv;             /* q / k columns (qkv_acc offsets)               */
+    int super_chunks;        /* long-context kernel (plan.long_ctx): one unit walks this
+                                many chunks with an online softmax (>= 1)           */
+    int pad_;
 } teal_step_attn;
 
 typedef struct teal_step_phase {
@@ -402,8 +405,10 @@ typedef struct teal_step_plan {
     long long* acc_zero;             /* LOAD: ACC accumulators zeroed each step */
     int64_t acc_zero_n;              /* (elements)                              */
     const teal_step_tp* tp;          /* nullable device pointer: fused tensor parallel     */
-    int noncoop, pad4_;              /* 1: ordinary launch (single-GPU TP validation runs the
-                                        ranks' launches concurrently on one device)       */
+    int noncoop, long_ctx;           /* noncoop 1: ordinary launch (single-GPU TP validation runs the
+                                        ranks' launches concurrently on one device);
+                                        long_ctx 1: the kernel variant whose attention units
+                                        walk attn.super_chunks chunks each (long contexts) */
     int phase_begin, phase_end;      /* this launch runs phases [begin, end) (end 0: all).
                                         Dependencies on earlier launches are met by stream
                                         order: the host drops them from the phase list

@@ -1233,6 +1233,177 @@ __device__ __noinline__ void attn_unit(const teal_step_plan& P, const teal_step_
 #undef ATT_STAMP
 }
 
+
+// Long-context attention unit (kernel variant long_ctx): unit (g, su) walks
+// chunks [su*S, su*S + S) with an online softmax — per chunk the staged K/V,
+// scores, running max / sum update (previous context rescaled by
+// exp(m_old - m_new)) — and writes ONE record for the S chunks, so a long
+// context has S x fewer units and records for the last arriver to combine.
+__device__ __noinline__ void attn_unit_multi(const teal_step_plan& P, const teal_step_attn& a, int g, int su, int L) {
+    Smem& s = smem();
+    constexpr int QO = ATT_MAXG * ATT_MAXHD / NT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = a.H / a.KVH, hd = a.hd, S = a.super_chunks;
+    const int nact = min(a.nchunks, (L + a.chunk - 1) / a.chunk);
+    const int nsu = (nact + S - 1) / S;
+    const int c0 = su * S, c1 = min(nact, c0 + S);
+    const int rec = G * hd + 2 * G;
+    float* my = a.partials + ((int64_t)g * a.nchunks + su) * rec;
+    const int64_t kvbase = (int64_t)g * a.max_seq * hd;
+    const int pos = L - 1;
+    const float rs = rsqrtf((float)hd);
+    const bool bf = a.kv_dtype == TEAL_BF16;
+    const int vpr = hd * (bf ? 2 : 4) / 16;
+    float accv[QO];
+#pragma unroll
+    for (int j = 0; j < QO; ++j) accv[j] = 0.f;
+#pragma unroll 1
+    for (int c = c0; c < c1; ++c) {
+        const int p0 = c * a.chunk, p1 = min(L, p0 + a.chunk), np = p1 - p0;
+        const int newrow = (a.qkv_acc && pos >= p0 && pos < p1) ? pos - p0 : -1;
+        attn_stage_kv(a, p0, np, newrow, kvbase);
+        if (c == c0) wait_range(P.counters, a.dep_base + g, a.dep_base + g, a.dep_target[g]);
+        attn_stage_q(a, g, pos, newrow, kvbase);
+        __syncthreads();
+#pragma unroll 1
+        for (int i = tid; i < G * np; i += NT) {
+            const int h = i / np, p = i - h * np;
+            const float4* qv = reinterpret_cast<const float4*>(s.u.a.q + h * hd);
+            const uint4* kv = s.u.a.k + p * (vpr + 1);
+            float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (bf) {
+#pragma unroll 2
+                for (int e = 0; e < vpr; ++e) {
+                    const uint4 y = kv[e];
+                    const float4 x0 = qv[2 * e], x1 = qv[2 * e + 1];
+                    acc4.x = fmaf(x0.x, bf16_lo(y.x), acc4.x);
+                    acc4.y = fmaf(x0.y, bf16_hi(y.x), acc4.y);
+                    acc4.z = fmaf(x0.z, bf16_lo(y.y), acc4.z);
+                    acc4.w = fmaf(x0.w, bf16_hi(y.y), acc4.w);
+                    acc4.x = fmaf(x1.x, bf16_lo(y.z), acc4.x);
+                    acc4.y = fmaf(x1.y, bf16_hi(y.z), acc4.y);
+                    acc4.z = fmaf(x1.z, bf16_lo(y.w), acc4.z);
+                    acc4.w = fmaf(x1.w, bf16_hi(y.w), acc4.w);
+                }
+            } else {
+#pragma unroll 2
+                for (int e = 0; e < vpr; ++e) {
+                    const uint4 y = kv[e];
+                    const float4 x = qv[e];
+                    acc4.x = fmaf(x.x, __uint_as_float(y.x), acc4.x);
+                    acc4.y = fmaf(x.y, __uint_as_float(y.y), acc4.y);
+                    acc4.z = fmaf(x.z, __uint_as_float(y.z), acc4.z);
+                    acc4.w = fmaf(x.w, __uint_as_float(y.w), acc4.w);
+                }
+            }
+            s.u.a.sc[h * ATT_MAXCHUNK + p] = ((acc4.x + acc4.y) + (acc4.z + acc4.w)) * rs;
+        }
+        __syncthreads();
+        // online softmax: warp per head; s.col[h] = rescale of the previous context
+#pragma unroll 1
+        for (int h = warp; h < G; h += NW) {
+            float mx = -INFINITY;
+            for (int p = lane; p < np; p += 32) mx = fmaxf(mx, s.u.a.sc[h * ATT_MAXCHUNK + p]);
+            mx = warp_max(mx);
+            const float mold = c == c0 ? -INFINITY : s.am[h];
+            const float mnew = fmaxf(mold, mx);
+            float l = 0.f;
+            for (int p = lane; p < np; p += 32) {
+                const float e = expf(s.u.a.sc[h * ATT_MAXCHUNK + p] - mnew);
+                s.u.a.sc[h * ATT_MAXCHUNK + p] = e;
+                l += e;
+            }
+            l = warp_sum(l);
+            if (lane == 0) {
+                const float sc = c == c0 ? 0.f : expf(mold - mnew);
+                s.col[h] = sc;
+                s.am[h] = mnew;
+                s.al[h] = (c == c0 ? 0.f : s.al[h] * sc) + l;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < QO; ++j) {
+            const int o = tid + j * NT;
+            if (o >= G * hd) continue;
+            const int h = o / hd, dd = o - h * hd;
+            const float* pr = s.u.a.sc + h * ATT_MAXCHUNK;
+            float x0 = 0.f, x1 = 0.f;
+            if (bf) {
+                const uint16_t* vc = reinterpret_cast<const uint16_t*>(s.u.a.v) + dd;
+                for (int p = 0; p + 1 < np; p += 2) {
+                    x0 = fmaf(pr[p], bf16_to_f32(vc[p * hd]), x0);
+                    x1 = fmaf(pr[p + 1], bf16_to_f32(vc[(p + 1) * hd]), x1);
+                }
+                if (np & 1) x0 = fmaf(pr[np - 1], bf16_to_f32(vc[(np - 1) * hd]), x0);
+            } else {
+                const float* vc = reinterpret_cast<const float*>(s.u.a.v) + dd;
+                for (int p = 0; p + 1 < np; p += 2) {
+                    x0 = fmaf(pr[p], vc[p * hd], x0);
+                    x1 = fmaf(pr[p + 1], vc[(p + 1) * hd], x1);
+                }
+                if (np & 1) x0 = fmaf(pr[np - 1], vc[(np - 1) * hd], x0);
+            }
+            accv[j] = fmaf(accv[j], s.col[h], x0 + x1);
+        }
+        __syncthreads();  // the next chunk's staging rewrites K/V, q and the scores
+    }
+    if (nsu == 1) {  // one unit holds every position: the context is final
+#pragma unroll
+        for (int j = 0; j < QO; ++j) {
+            const int o = tid + j * NT;
+            if (o < G * hd) a.ctx[(int64_t)g * G * hd + o] = accv[j] / s.al[o / hd];
+        }
+        signal(P.counters, a.sig_base + g, a.sig_base + g);
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < QO; ++j) {
+        const int o = tid + j * NT;
+        if (o < G * hd) __stcg(my + o, accv[j]);
+    }
+    if (tid < G) {
+        __stcg(my + G * hd + tid, s.am[tid]);
+        __stcg(my + G * hd + G + tid, s.al[tid]);
+    }
+    if (!take_ticket(a.tickets + g, (unsigned)nsu - 1u, s.last)) return;
+    const float* rb = a.partials + (int64_t)g * a.nchunks * rec;
+    for (int q = tid; q < nsu * 2 * G; q += NT) {  // (m, l) of every record -> smem
+        const int c = q / (2 * G), k = q % (2 * G);
+        s.u.a.sc[q] = __ldcg(rb + (int64_t)c * rec + G * hd + k);
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int o = tid; o < G * hd; o += NT) {
+        const int h = o / hd;
+        float M = -INFINITY;
+        for (int c = 0; c < nsu; ++c)
+            if (s.u.a.sc[c * 2 * G + G + h] > 0.f) M = fmaxf(M, s.u.a.sc[c * 2 * G + h]);
+        float num = 0.f, dn = 0.f;
+#pragma unroll 1
+        for (int cb = 0; cb < nsu; cb += 16) {  // 16 records in flight (clamped indices)
+            float pv[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) pv[q] = __ldcg(rb + (int64_t)(cb + q < nsu ? cb + q : 0) * rec + o);
+#pragma unroll 1
+            for (int q = 0; q < 16; ++q) {
+                const int c = cb + q;
+                if (c < nsu) {
+                    const float ls = s.u.a.sc[c * 2 * G + G + h];
+                    if (ls > 0.f) {
+                        const float sc = expf(s.u.a.sc[c * 2 * G + h] - M);
+                        num = fmaf(pv[q], sc, num);
+                        dn = fmaf(ls, sc, dn);
+                    }
+                }
+            }
+        }
+        a.ctx[(int64_t)g * G * hd + o] = num / dn;
+    }
+    signal(P.counters, a.sig_base + g, a.sig_base + g);
+}
+
+template <bool LC>
 __device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, Smem& s) {
     const teal_step_attn& a = P.attns[ph.group];
     // the sequence length is written by this step's load phase: a CTA that had
@@ -1244,14 +1415,15 @@ __device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, S
     }
     const int L = __ldcg(P.state + 1);
     const int nact = min(a.nchunks, (L + a.chunk - 1) / a.chunk);  // chunks holding positions
-    const int nu = a.KVH * nact;
+    const int nu = LC ? a.KVH * ((nact + a.super_chunks - 1) / a.super_chunks) : a.KVH * nact;
     const int G = gridDim.x;
     // unit u = (chunk u / KVH, kv group u % KVH) runs on CTA G-1 - (u*G)/nu:
     // spread over the grid from its end (the qkv phase leaves the last CTAs idle)
     const int cr = G - 1 - (int)blockIdx.x;
     for (int u = (int)(((int64_t)cr * nu + G - 1) / G); u < nu && (int64_t)u * G / nu == cr; ++u) {
         const int g = u % a.KVH, ch = u / a.KVH;  // (the unit waits for its q/k/v tiles itself)
-        attn_unit(P, a, g, ch, L);
+        if constexpr (LC) attn_unit_multi(P, a, g, ch, L);
+        else attn_unit(P, a, g, ch, L);
         __syncthreads();
     }
 }
@@ -1351,7 +1523,7 @@ __device__ void resid_phase(const teal_step_plan& P, const teal_step_phase& ph, 
 
 // MINB resident CTAs per SM (register budget 65536 / (NT * MINB)); UB rows in
 // flight per warp per pipeline stage.
-template <int WT, int MINB, int UB>
+template <int WT, int MINB, int UB, bool LC = false>
 __global__ void __launch_bounds__(NT, MINB) step_kernel(const __grid_constant__ teal_step_plan P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
@@ -1363,7 +1535,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const __grid_constant__ 
         unsigned long long* tl = P.timeline ? P.timeline + ((int64_t)blockIdx.x * P.nphases + p) * 8 : nullptr;
         if (tl && tid == 0) tl[0] = gtimer();
         if (ph.kind == TEAL_PHASE_GEMV) gemv_slice_t<WT, UB>(P, ph, P.groups[ph.group], s, pol, tl);
-        else if (ph.kind == TEAL_PHASE_ATTN) attn_phase(P, ph, s);
+        else if (ph.kind == TEAL_PHASE_ATTN) attn_phase<LC>(P, ph, s);
         else if (ph.kind == TEAL_PHASE_RESID) resid_phase(P, ph, P.groups[ph.group]);
         else load_phase(P);
         __syncthreads();
@@ -1402,17 +1574,18 @@ static int occ_mode() {
 }
 
 template <int WT>
-static void* kernel_ptr_t() {
+static void* kernel_ptr_t(bool lc) {
+    if (lc) return (void*)step_kernel<WT, 2, 6, true>;
     if (occ_mode() == 2) return (void*)step_kernel<WT, 2, 6>;
     return (void*)step_kernel<WT, 3, 4>;
 }
 
-static void* kernel_ptr(int w_dtype) {
+static void* kernel_ptr(int w_dtype, bool lc = false) {
     switch (w_dtype) {
-        case TEAL_BF16: return kernel_ptr_t<TEAL_BF16>();
-        case TEAL_I8: return kernel_ptr_t<TEAL_I8>();
-        case TEAL_I4: return kernel_ptr_t<TEAL_I4>();
-        default: return kernel_ptr_t<TEAL_F32>();
+        case TEAL_BF16: return kernel_ptr_t<TEAL_BF16>(lc);
+        case TEAL_I8: return kernel_ptr_t<TEAL_I8>(lc);
+        case TEAL_I4: return kernel_ptr_t<TEAL_I4>(lc);
+        default: return kernel_ptr_t<TEAL_F32>(lc);
     }
 }
 
@@ -1594,7 +1767,15 @@ int teal_step_launch(const teal_step_plan* p, cudaStream_t stream) {
     cfg.attrs = attr;
     cfg.numAttrs = p->noncoop ? 0 : 1;
     void* args[1] = {(void*)p};
-    cudaLaunchKernelExC(&cfg, kernel_ptr(p->w_dtype), args);
+    const void* k = kernel_ptr(p->w_dtype, p->long_ctx != 0);
+    if (p->long_ctx) {  // (the default variant gets its attribute in occupancy())
+        static bool lc_attr[4] = {false, false, false, false};
+        if (!lc_attr[p->w_dtype & 3]) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+            lc_attr[p->w_dtype & 3] = true;
+        }
+    }
+    cudaLaunchKernelExC(&cfg, k, args);
     return check_launch("teal_step_launch");
 }
 

@@ -57,7 +57,8 @@ class StepAttn(ctypes.Structure):
     _fields_ = [("q", c_vp), ("k_cache", c_vp), ("v_cache", c_vp), ("ctx", c_vp), ("partials", c_vp),
                 ("tickets", c_vp), ("max_seq", c_i64), ("H", c_i), ("KVH", c_i), ("hd", c_i), ("kv_dtype", c_i),
                 ("chunk", c_i), ("nchunks", c_i), ("sig_base", c_i), ("dep_base", c_i), ("dep_target", c_vp),
-                ("dbg", c_vp), ("qkv_acc", c_vp), ("rope_cos", c_vp), ("rope_sin", c_vp), ("nq", c_i), ("nkv", c_i)]
+                ("dbg", c_vp), ("qkv_acc", c_vp), ("rope_cos", c_vp), ("rope_sin", c_vp), ("nq", c_i), ("nkv", c_i),
+                ("super_chunks", c_i), ("pad_", c_i)]
 
 
 class StepPhase(ctypes.Structure):
@@ -70,7 +71,7 @@ class StepPlan(ctypes.Structure):
                 ("cand_v", c_vp), ("cand_i", c_vp), ("token_out", c_vp), ("lm_done", c_vp), ("timeline", c_vp),
                 ("nphases", c_i), ("ncounters", c_i), ("prefetch_bytes", c_i), ("pad_", c_i),
                 ("d", c_i), ("emb_dtype", c_i), ("w_dtype", c_i), ("ctas", c_i),
-                ("acc_zero", c_vp), ("acc_zero_n", c_i64), ("tp", c_vp), ("noncoop", c_i), ("pad4_", c_i),
+                ("acc_zero", c_vp), ("acc_zero_n", c_i64), ("tp", c_vp), ("noncoop", c_i), ("long_ctx", c_i),
                 ("phase_begin", c_i), ("phase_end", c_i)]
 
 
@@ -361,7 +362,7 @@ class StepDecoder:
     def __init__(self, weights, thresholds=None, kv_dtype=None, device=None,
                  taps: bool = False, attn_chunk: int = 0, ctas: int = 0,
                  count_kept: bool = False, attn_debug: bool = False, prefetch_kb: int | None = None,
-                 quant: str | None = None):
+                 quant: str | None = None, long_context: int = 0):
         self.w = weights
         spec = self.spec = weights.spec
         dev = self.device = device or RT.require_cuda()
@@ -421,6 +422,9 @@ class StepDecoder:
         else:
             self.rope_cos = self.rope_sin = None
         self.attn_chunk = attn_chunk
+        # long_context = S > 1: the kernel variant whose attention units each walk
+        # S chunks with an online softmax (fewer units and records at long context)
+        self.super_chunks = int(long_context) if long_context and long_context > 1 else 1
         self.nchunks = -(-spec.max_seq // attn_chunk)
         self.taps = StepTaps() if taps else None
         if taps:
@@ -544,7 +548,8 @@ class StepDecoder:
                                   self.ws["attn"].data_ptr(), self.tk["attn"].data_ptr(), spec.max_seq,
                                   spec.n_heads, KVH, hd, RT.dtype_code(self.kv_dtype), self.attn_chunk,
                                   self.nchunks, cb["odep"], cb["attn"], tgt.data_ptr(), RT.ptr(self.attn_dbg),
-                                  A["qkv"].data_ptr(), RT.ptr(self.rope_cos), RT.ptr(self.rope_sin), nq, nkv))
+                                  A["qkv"].data_ptr(), RT.ptr(self.rope_cos), RT.ptr(self.rope_sin), nq, nkv,
+                                  max(1, self.super_chunks), 0))
             phases.append(StepPhase(PHASE_ATTN, len(attns) - 1, DEP_GLOBAL, 0, Gc, 1))  # step state from the load
             # --- o: rows = context channels, each waits for its kv group's context
             tv = _t32(t[3])
@@ -652,6 +657,7 @@ class StepDecoder:
                                                       self.token.data_ptr(), self.lm_done.data_ptr())
         p.nphases, p.ncounters, p.d = self.nphases, self.ncounters, d
         p.w_dtype, p.ctas = self.w_code, self.grid
+        p.long_ctx = int(self.super_chunks > 1)
         p.prefetch_bytes = self.prefetch_bytes
         self.plan = p
 

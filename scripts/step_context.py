@@ -31,3 +31,24 @@ for pos in (64, 512, 1024, 2048, 4096, 8000):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 20
     print(f"context ~{pos + 13:5d}: {ms:.3f} ms/token  {1e3 / ms:.1f} tok/s", flush=True)
+
+# the long-context kernel variant: units walk 4 chunks with an online softmax
+del dec
+torch.cuda.empty_cache()
+dec = E.StepDecoder(W, thr, long_context=4)
+for pos in (64, 512, 1024, 2048, 4096, 8000):
+    dec.reset(pos)
+    dec.token.fill_(1)
+    dec.capture()
+    dec.reset(pos)
+    for _ in range(3):
+        dec.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        dec.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 20
+    print(f"long_context=4 context ~{pos + 13:5d}: {ms:.3f} ms/token  {1e3 / ms:.1f} tok/s", flush=True)
