@@ -362,7 +362,7 @@ class StepDecoder:
     def __init__(self, weights, thresholds=None, kv_dtype=None, device=None,
                  taps: bool = False, attn_chunk: int = 0, ctas: int = 0,
                  count_kept: bool = False, attn_debug: bool = False, prefetch_kb: int | None = None,
-                 quant: str | None = None, long_context: int = 0):
+                 quant: str | None = None, long_context: int = 0, long_from: int = 2048):
         self.w = weights
         spec = self.spec = weights.spec
         dev = self.device = device or RT.require_cuda()
@@ -422,9 +422,13 @@ class StepDecoder:
         else:
             self.rope_cos = self.rope_sin = None
         self.attn_chunk = attn_chunk
-        # long_context = S > 1: the kernel variant whose attention units each walk
-        # S chunks with an online softmax (fewer units and records at long context)
+        # long_context = S > 1: from position `long_from` on, steps run the kernel
+        # variant whose attention units each walk S chunks with an online
+        # softmax (fewer units and records; slower below ~2 K positions)
         self.super_chunks = int(long_context) if long_context and long_context > 1 else 1
+        self.long_from = int(long_from)
+        self._pos = 0
+        self.graph_long = None
         self.nchunks = -(-spec.max_seq // attn_chunk)
         self.taps = StepTaps() if taps else None
         if taps:
@@ -657,7 +661,7 @@ class StepDecoder:
                                                       self.token.data_ptr(), self.lm_done.data_ptr())
         p.nphases, p.ncounters, p.d = self.nphases, self.ncounters, d
         p.w_dtype, p.ctas = self.w_code, self.grid
-        p.long_ctx = int(self.super_chunks > 1)
+        p.long_ctx = 0  # chosen per launch (_use_long)
         p.prefetch_bytes = self.prefetch_bytes
         self.plan = p
 
@@ -709,6 +713,7 @@ class StepDecoder:
     # -- step -----------------------------------------------------------------
     def reset(self, start_pos: int = 0) -> None:
         self.state.copy_(torch.tensor([start_pos - 1, start_pos], dtype=torch.int32))
+        self._pos = start_pos
         if start_pos == 0:
             self.kcache.zero_()
             self.vcache.zero_()
@@ -739,8 +744,12 @@ class StepDecoder:
         total += positions * spec.n_layers * 2 * spec.n_kv * kvb
         return total
 
-    def _launch(self, stream_h: int, from_token: bool) -> None:
+    def _use_long(self) -> bool:
+        return self.super_chunks > 1 and self._pos >= self.long_from
+
+    def _launch(self, stream_h: int, from_token: bool, long_ctx: bool | None = None) -> None:
         p = self.plan
+        p.long_ctx = int(self._use_long() if long_ctx is None else long_ctx)
         if from_token:
             p.emb = self.w.embedding.data_ptr()
         else:
@@ -753,13 +762,15 @@ class StepDecoder:
         else:
             self.x_in.copy_(torch.from_numpy(np.ascontiguousarray(x_row, dtype=np.float32)), non_blocking=True)
         self._launch(RT.stream_handle(), from_token=False)
+        self._pos += 1
         return self.x
 
     def step_token(self) -> torch.Tensor:
         if self.graph is not None:
-            self.graph.replay()
+            self.replay()
         else:
             self._launch(RT.stream_handle(), from_token=True)
+            self._pos += 1
         return self.token
 
     def step_token_host(self, tok_in: torch.Tensor, tok_out: torch.Tensor) -> None:
@@ -768,15 +779,22 @@ class StepDecoder:
         tok_out.copy_(self.token, non_blocking=True)
 
     def capture(self, from_token: bool = True) -> torch.cuda.CUDAGraph:
-        s = torch.cuda.Stream(device=self.device)
-        s.wait_stream(torch.cuda.current_stream())
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(s):
-            with torch.cuda.graph(g, stream=s):
-                self._launch(s.cuda_stream, from_token)
-        torch.cuda.current_stream().wait_stream(s)
-        self.graph = g
-        return g
+        """One CUDA graph of the step launch (and, with long_context, a second
+        one of the long-context variant; replay() picks by position)."""
+        graphs = []
+        for lc in ((False, True) if self.super_chunks > 1 else (False,)):
+            s = torch.cuda.Stream(device=self.device)
+            s.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    self._launch(s.cuda_stream, from_token, long_ctx=lc)
+            torch.cuda.current_stream().wait_stream(s)
+            graphs.append(g)
+        self.graph = graphs[0]
+        self.graph_long = graphs[1] if len(graphs) > 1 else None
+        return self.graph
 
     def replay(self) -> None:
-        self.graph.replay()
+        (self.graph_long if self._use_long() and self.graph_long is not None else self.graph).replay()
+        self._pos += 1

@@ -221,3 +221,27 @@ def test_long_context_variant_matches_default(super_chunks):
         assert rel_err(dec.x.cpu().numpy(), x_ref.cpu().numpy()) < 1e-3, i
         assert int(dec.token.item()) == int(torch.argmax(logits_ref).item()) or \
             rel_err(dec.logits.cpu().numpy(), logits_ref.cpu().numpy()) < 1e-3, i
+
+
+def test_long_context_switches_by_position():
+    # long_context with a switch position: the first steps run the default
+    # kernel, later ones the multi-chunk variant (eager and graph replay)
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200 import engine as E
+    from test_decode_gpu import torch_decode_reference
+    spec = D.DecoderSpec(1024, 8, 2, 2816, 2, vocab=1000, rope_theta=500000.0, norm_eps=1e-5, max_seq=128)
+    W = D.random_weights(spec, torch.bfloat16, seed=3)
+    thr = [[0.3, 0.4, 0.5, 0.02, 0.6, 0.7, 0.05]] * 2
+    tokens = [5, 17, 999, 3, 250, 7, 7, 42, 11, 600] * 6
+    ref = torch_decode_reference(W, thr, tokens, spec, torch.float32)
+    for graph in (False, True):
+        dec = E.StepDecoder(W, thr, kv_dtype=torch.float32, attn_chunk=16, long_context=2, long_from=30)
+        dec.reset()
+        if graph:
+            dec.capture()
+            dec.reset()
+        for i, tok in enumerate(tokens):
+            dec.token.fill_(tok)
+            dec.step_token()
+            torch.cuda.synchronize()
+            assert rel_err(dec.x.cpu().numpy(), ref[i][0].cpu().numpy()) < 1e-3, (graph, i)
