@@ -1143,35 +1143,66 @@ __device__ __noinline__ void attn_unit(const teal_step_plan& P, const teal_step_
             if (lane == 0) { s.am[h] = mx; s.al[h] = l; }
         }
         __syncthreads();
-        // context partial: thread -> (head, d), positions ascending in two
-        // chains (even / odd).  A single chunk holding every position is
-        // final: normalise and write the context (no record, ticket, combine).
+        // context partial: thread -> (head, pair of dims), positions in four
+        // independent chains (p mod 4, summed (0+1)+(2+3)) so the chain depth
+        // is np/4; 32-bit V loads (bf16 pair) / 64-bit (fp32 pair), the
+        // probabilities as float4 broadcasts.  A single chunk holding every
+        // position is final: normalise and write the context (no record,
+        // ticket, combine).
         const bool single = (p0 == 0 && p1 == L);
+        const int hp = hd >> 1;
 #pragma unroll 1
-        for (int o = tid; o < G * hd; o += NT) {
-            const int h = o / hd, dd = o - h * hd;
+        for (int o = tid; o < G * hp; o += NT) {
+            const int h = o / hp, dp = o - h * hp;
             const float* pr = s.u.a.sc + h * ATT_MAXCHUNK;
-            float c0 = 0.f, c1 = 0.f;
+            float cx[4] = {0.f, 0.f, 0.f, 0.f}, cy[4] = {0.f, 0.f, 0.f, 0.f};
+            int p = 0;
             if (bf) {
-                const uint16_t* vc = reinterpret_cast<const uint16_t*>(s.u.a.v) + dd;
-#pragma unroll 4
-                for (int p = 0; p + 1 < np; p += 2) {
-                    c0 = fmaf(pr[p], bf16_to_f32(vc[p * hd]), c0);
-                    c1 = fmaf(pr[p + 1], bf16_to_f32(vc[(p + 1) * hd]), c1);
+                const uint32_t* vc = reinterpret_cast<const uint32_t*>(s.u.a.v) + dp;
+#pragma unroll 2
+                for (; p + 3 < np; p += 4) {
+                    const float4 pp = *reinterpret_cast<const float4*>(pr + p);
+                    const uint32_t u0 = vc[p * hp], u1 = vc[(p + 1) * hp], u2 = vc[(p + 2) * hp], u3 = vc[(p + 3) * hp];
+                    cx[0] = fmaf(pp.x, bf16_lo(u0), cx[0]); cy[0] = fmaf(pp.x, bf16_hi(u0), cy[0]);
+                    cx[1] = fmaf(pp.y, bf16_lo(u1), cx[1]); cy[1] = fmaf(pp.y, bf16_hi(u1), cy[1]);
+                    cx[2] = fmaf(pp.z, bf16_lo(u2), cx[2]); cy[2] = fmaf(pp.z, bf16_hi(u2), cy[2]);
+                    cx[3] = fmaf(pp.w, bf16_lo(u3), cx[3]); cy[3] = fmaf(pp.w, bf16_hi(u3), cy[3]);
                 }
-                if (np & 1) c0 = fmaf(pr[np - 1], bf16_to_f32(vc[(np - 1) * hd]), c0);
+#pragma unroll
+                for (int k = 0; k < 3; ++k)  // tail (< 4 positions): chain k
+                    if (p + k < np) {
+                        const uint32_t u = vc[(p + k) * hp];
+                        cx[k] = fmaf(pr[p + k], bf16_lo(u), cx[k]);
+                        cy[k] = fmaf(pr[p + k], bf16_hi(u), cy[k]);
+                    }
             } else {
-                const float* vc = reinterpret_cast<const float*>(s.u.a.v) + dd;
-#pragma unroll 4
-                for (int p = 0; p + 1 < np; p += 2) {
-                    c0 = fmaf(pr[p], vc[p * hd], c0);
-                    c1 = fmaf(pr[p + 1], vc[(p + 1) * hd], c1);
+                const float2* vc = reinterpret_cast<const float2*>(s.u.a.v) + dp;
+#pragma unroll 2
+                for (; p + 3 < np; p += 4) {
+                    const float4 pp = *reinterpret_cast<const float4*>(pr + p);
+                    const float2 u0 = vc[p * hp], u1 = vc[(p + 1) * hp], u2 = vc[(p + 2) * hp], u3 = vc[(p + 3) * hp];
+                    cx[0] = fmaf(pp.x, u0.x, cx[0]); cy[0] = fmaf(pp.x, u0.y, cy[0]);
+                    cx[1] = fmaf(pp.y, u1.x, cx[1]); cy[1] = fmaf(pp.y, u1.y, cy[1]);
+                    cx[2] = fmaf(pp.z, u2.x, cx[2]); cy[2] = fmaf(pp.z, u2.y, cy[2]);
+                    cx[3] = fmaf(pp.w, u3.x, cx[3]); cy[3] = fmaf(pp.w, u3.y, cy[3]);
                 }
-                if (np & 1) c0 = fmaf(pr[np - 1], vc[(np - 1) * hd], c0);
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    if (p + k < np) {
+                        const float2 u = vc[(p + k) * hp];
+                        cx[k] = fmaf(pr[p + k], u.x, cx[k]);
+                        cy[k] = fmaf(pr[p + k], u.y, cy[k]);
+                    }
             }
-            const float r = c0 + c1;
-            if (single) a.ctx[(int64_t)g * G * hd + o] = r / s.al[h];
-            else __stcg(my + o, r);
+            float2 r = make_float2((cx[0] + cx[1]) + (cx[2] + cx[3]), (cy[0] + cy[1]) + (cy[2] + cy[3]));
+            const int oo = h * hd + 2 * dp;
+            if (single) {
+                r.x = r.x / s.al[h];
+                r.y = r.y / s.al[h];
+                *reinterpret_cast<float2*>(a.ctx + (int64_t)g * G * hd + oo) = r;
+            } else {
+                __stcg(reinterpret_cast<float2*>(my + oo), r);
+            }
         }
         if (single) {
             ATT_STAMP(3);
