@@ -21,9 +21,10 @@
 // columns of a TC = 32*CPL column tile and all B batch rows (fp32
 // accumulators acc[B][CPL]); warps take kept rows round-robin with U rows in
 // flight; warps are reduced in fixed order, split tiles by the last-arriving
-// CTA in ascending-CTA order (deterministic).  CUDA cores only: at B >= 4 the
-// kernel is FMA-bound, at B = 1 the fused single-row kernels
-// are the fast path.
+// CTA in ascending-CTA order (deterministic).  The FMA kernel (CUDA cores)
+// serves int8 / int4 rows and B < 4; bf16 rows at B >= 4 (where the FMA loop
+// is issue-bound, 2*B flops per weight element) run the mma.sync variant
+// below.  At B = 1 the fused single-row kernels are the fast path.
 #include "teal_common.cuh"
 #include <string.h>
 
@@ -306,12 +307,237 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_kernel(const __grid_consta
     if (A.kept && lane == 0 && kcount) atomicAdd(A.kept, (unsigned long long)kcount);
 }
 
+
+// ---- bf16 rows, B >= 4: tensor-core (mma.sync m16n8k16) variant ----------
+// Same decomposition, mask and deterministic split-K combine as above; the
+// per-row FMA loop (FMA-issue bound at B >= 4: 2*B flops per weight element)
+// is replaced by warp MMAs over the chunk's gathered rows:
+//   D[b][col] += sum_k X[b][k] * W[idx_k][col]   (M = batch padded to 16,
+//   N = 32 columns per warp, K = kept rows of the chunk in steps of 16).
+// Kept rows' TCM-column slices are gathered into shared memory with
+// cp.async (16 B per request, zero-filled past n), row stride padded by 16 B
+// so ldmatrix(.trans) phases are bank-conflict free.  X is fp32: it is split
+// exactly into three bf16 terms x = h1 + h2 + h3 (h_i = RN(x - h_1 - ...)),
+// each product with a bf16 weight is exact in fp32, so the result matches an
+// fp32 GEMV to accumulation rounding (the rel 1e-5 bar of the FMA kernel).
+constexpr int MC = 128;               // candidate rows per chunk
+constexpr int TCM = 256;              // columns per tile: 8 warps x 32
+constexpr int WSTR = TCM * 2 + 16;    // staged row stride (bytes)
+constexpr int XSTR = MC * 2 + 16;     // staged x row stride (bytes): [b][k]
+constexpr int NSPLIT = 3;
+constexpr size_t kMmaW = (size_t)MC * WSTR;
+constexpr size_t kMmaX = (size_t)NSPLIT * 16 * XSTR;
+constexpr size_t kMmaSmem = kMmaW + kMmaX + MC * 4 + NW * 4 + 16;
+static_assert((size_t)16 * TCM * 4 <= kMmaW, "combine buffer aliases the row stage");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_constant__ KP P) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    unsigned char* s_w = sm;                                // [MC][WSTR]
+    unsigned char* s_xb = sm + kMmaW;                       // [NSPLIT][16][XSTR]
+    int* s_idx = reinterpret_cast<int*>(sm + kMmaW + kMmaX);
+    int* s_wcnt = s_idx + MC;
+    int* s_last = s_wcnt + NW;
+    float* s_red = reinterpret_cast<float*>(sm);            // [16][TCM], after the last chunk
+    const teal_gemv_batched_args& A = P.a;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x;
+    const int64_t g0 = (int64_t)c * P.F / P.G, g1 = (int64_t)(c + 1) * P.F / P.G;
+    const int B = A.B;
+    const uint16_t* W = reinterpret_cast<const uint16_t*>(A.w);
+    unsigned kcount = 0;
+    const int mi = lane >> 3, mr = lane & 7;  // ldmatrix: matrix / row this lane addresses
+    for (int64_t gs = g0; gs < g1;) {
+        const int tile = (int)(gs / P.gpt);
+        const int64_t ge = min64(g1, (int64_t)(tile + 1) * P.gpt);
+        const int r0 = (int)(gs - (int64_t)tile * P.gpt) * 32;
+        const int r1 = (int)min64(A.m, (ge - (int64_t)tile * P.gpt) * 32);
+        gs = ge;
+        const int64_t tcol0 = (int64_t)tile * TCM;
+        float acc[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[j][q] = 0.f;
+        for (int ra = r0; ra < r1; ra += MC) {
+            const int rb = min(r1, ra + MC);
+            // shared mask of the chunk (threads 0..MC-1 own one row each)
+            const int i = ra + tid;
+            const bool v = tid < MC && i < rb;
+            float xs[BMAX];
+            float sabs = 0.f;
+#pragma unroll
+            for (int b = 0; b < BMAX; ++b) xs[b] = __ldg(A.x + (int64_t)(b < B ? b : 0) * A.m + (v ? i : ra));
+#pragma unroll
+            for (int b = 0; b < BMAX; ++b) {
+                xs[b] = (v && b < B) ? xs[b] : 0.f;
+                if (b < B) sabs = __fadd_rn(sabs, fabsf(xs[b]));
+            }
+            const float mean = (float)__ddiv_rn((double)sabs, (double)B);
+            const bool keep = v && !(mean <= A.t32);
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (tile == 0) {
+                if (A.mask && v) A.mask[i] = keep ? 0 : 1;
+                kcount += (lane == 0) ? __popc(bal) : 0u;
+            }
+            if (lane == 0) s_wcnt[warp] = __popc(bal);
+            __syncthreads();
+            int off = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const int cw = s_wcnt[w];
+                off += (w < warp) ? cw : 0;
+                tot += cw;
+            }
+            const int kpad = (tot + 15) & ~15;
+            // slot of this thread's row: kept rows first (ascending), then the
+            // pad slots [tot, kpad) take zero x and a valid (finite) row
+            int slot = -1;
+            if (keep) slot = off + __popc(bal & ((1u << lane) - 1u));
+            else if (tid >= MC && tid - MC < kpad - tot) slot = tot + (tid - MC);  // row-less threads
+            if (slot >= 0) {
+                s_idx[slot] = keep ? i : ra;
+#pragma unroll
+                for (int b = 0; b < 16; ++b) {
+                    const float x0 = keep ? xs[b] : 0.f;
+                    const uint16_t h1 = f32_to_bf16_rn(x0);
+                    const float e1 = x0 - __uint_as_float((uint32_t)h1 << 16);
+                    const uint16_t h2 = f32_to_bf16_rn(e1);
+                    const float e2 = e1 - __uint_as_float((uint32_t)h2 << 16);
+                    const uint16_t h3 = f32_to_bf16_rn(e2);
+                    *reinterpret_cast<uint16_t*>(s_xb + (0 * 16 + b) * XSTR + slot * 2) = h1;
+                    *reinterpret_cast<uint16_t*>(s_xb + (1 * 16 + b) * XSTR + slot * 2) = h2;
+                    *reinterpret_cast<uint16_t*>(s_xb + (2 * 16 + b) * XSTR + slot * 2) = h3;
+                }
+            }
+            __syncthreads();
+            if (kpad == 0) continue;  // uniform: nothing kept in this chunk
+            // gather the kept rows' tile slices (16 B per request, zero past n)
+            for (int q = tid; q < kpad * (TCM / 8); q += NT) {
+                const int k = q / (TCM / 8), sg = q % (TCM / 8);
+                const int64_t col = tcol0 + sg * 8;
+                const bool inb = col < A.n;
+                const uint16_t* src = W + (int64_t)s_idx[k] * A.ldw + (inb ? col : 0);
+                cp_async16(smem_u32(s_w + k * WSTR + sg * 16), src, inb ? 16 : 0);
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+            const uint32_t xb = smem_u32(s_xb), wb = smem_u32(s_w);
+            const int n0 = warp * 32;
+#pragma unroll 1
+            for (int k0 = 0; k0 < kpad; k0 += 16) {
+                uint32_t bf[2][4];
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj)
+                    ldsm_x4_t(wb + (k0 + mr + 8 * (mi & 1)) * WSTR + (n0 + jj * 16 + 8 * (mi >> 1)) * 2,
+                              bf[jj][0], bf[jj][1], bf[jj][2], bf[jj][3]);
+#pragma unroll
+                for (int sp = 0; sp < NSPLIT; ++sp) {
+                    uint32_t af[4];
+                    ldsm_x4(xb + (sp * 16 + mr + 8 * (mi & 1)) * XSTR + (k0 + 8 * (mi >> 1)) * 2, af[0], af[1], af[2], af[3]);
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj) {
+                        mma_bf16(acc[2 * jj], af, bf[jj][0], bf[jj][1]);
+                        mma_bf16(acc[2 * jj + 1], af, bf[jj][2], bf[jj][3]);
+                    }
+                }
+            }
+            __syncthreads();  // the stage is rewritten by the next chunk
+        }
+        // warp-owned columns: D fragment -> s_red[b][col] (no cross-warp sum)
+        {
+            const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int col = warp * 32 + j * 8 + 2 * tq;
+                s_red[gq * TCM + col] = acc[j][0];
+                s_red[gq * TCM + col + 1] = acc[j][1];
+                s_red[(gq + 8) * TCM + col] = acc[j][2];
+                s_red[(gq + 8) * TCM + col + 1] = acc[j][3];
+            }
+        }
+        __syncthreads();
+        // split-K combine (ascending CTA order) + store, as the FMA kernel
+        const int cf = owner_of((int64_t)tile * P.gpt, P.F, P.G);
+        const int cl = owner_of((int64_t)(tile + 1) * P.gpt - 1, P.F, P.G);
+        bool fin = true;
+        if (cl > cf) {
+            float* slot = A.ws + ((int64_t)tile * P.maxc + (c - cf)) * (16 * TCM);
+            for (int q = tid; q < B * TCM; q += NT) __stcg(slot + q, s_red[q]);
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                const unsigned prev = atomicAdd(A.tickets + tile, 1u);
+                *s_last = prev == (unsigned)(cl - cf);
+                if (*s_last) {
+                    A.tickets[tile] = 0u;
+                    __threadfence();
+                }
+            }
+            __syncthreads();
+            fin = *s_last != 0;
+            if (fin) {
+                const float* base = A.ws + (int64_t)tile * P.maxc * (16 * TCM);
+                const int nc = cl - cf + 1;
+                for (int q = tid; q < B * TCM; q += NT) {
+                    float v = 0.f;
+                    for (int k0 = 0; k0 < nc; k0 += 16) {
+                        float pv[16];
+#pragma unroll
+                        for (int k = 0; k < 16; ++k)
+                            pv[k] = __ldcg(base + (int64_t)(k0 + k < nc ? k0 + k : 0) * (16 * TCM) + q);
+#pragma unroll
+                        for (int k = 0; k < 16; ++k)
+                            if (k0 + k < nc) v += pv[k];
+                    }
+                    s_red[q] = v;
+                }
+                __syncthreads();
+            }
+        }
+        if (fin) {
+            for (int q = tid; q < B * TCM; q += NT) {
+                const int b = q / TCM, cc = q - b * TCM;
+                const int64_t col = tcol0 + cc;
+                if (col < A.n) A.y[(int64_t)b * A.n + col] = s_red[b * TCM + cc];
+            }
+        }
+        __syncthreads();
+    }
+    if (A.kept && lane == 0 && kcount) atomicAdd(A.kept, (unsigned long long)kcount);
+}
+
+// Narrow outputs at B > 8 (few 256-column tiles: many split-K contributors
+// per tile and a long combine) stay on the FMA kernel's 128-column tiles.
+static bool use_mma(const teal_gemv_batched_args* a) {
+    return a->w_dtype == TEAL_BF16 && a->B >= 4 && a->n % 8 == 0 && a->ldw % 8 == 0 && (a->B <= 8 || a->n >= 4096);
+}
+
 static int cpl_of(int B) { return B > 8 ? 4 : 8; }
 static int tc_of(int B) { return 32 * cpl_of(B); }
 static int bm_of(int B) { return B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : B <= 8 ? 8 : 16; }
 
 static int plan(const teal_gemv_batched_args* a, KP* P) {
-    const int tc = tc_of(a->B);
+    const int tc = use_mma(a) ? TCM : tc_of(a->B);
     P->ntiles = (int)((a->n + tc - 1) / tc);
     P->gpt = (int)((a->m + 31) / 32);
     P->F = (int64_t)P->ntiles * P->gpt;
@@ -381,7 +607,8 @@ int teal_gemv_batched_workspace(const teal_gemv_batched_args* a, int* ctas, int6
     memset(&P, 0, sizeof(P));
     plan(a, &P);
     if (ctas) *ctas = P.G;
-    if (ws_floats) *ws_floats = (int64_t)P.ntiles * P.maxc * bm_of(a->B) * tc_of(a->B);
+    if (ws_floats) *ws_floats = use_mma(a) ? (int64_t)P.ntiles * P.maxc * 16 * TCM
+                                           : (int64_t)P.ntiles * P.maxc * bm_of(a->B) * tc_of(a->B);
     if (tickets) *tickets = P.ntiles;
     return TEAL_OK;
 }
@@ -394,6 +621,16 @@ int teal_gemv_batched(const teal_gemv_batched_args* a, cudaStream_t stream) {
     P.a = *a;
     plan(a, &P);
     TEAL_REQUIRE(P.G == 1 || P.maxc == 1 || (a->ws && a->tickets), "teal_gemv_batched: ws and tickets are required");
+    if (use_mma(a)) {
+        static bool attr = false;
+        if (!attr) {
+            if (cudaFuncSetAttribute(gemv_batched_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem) != cudaSuccess)
+                return check_launch("teal_gemv_batched (smem attribute)");
+            attr = true;
+        }
+        gemv_batched_mma_kernel<<<P.G, NT, kMmaSmem, stream>>>(P);
+        return check_launch("teal_gemv_batched");
+    }
     if (a->w_dtype == TEAL_BF16) return launch_w<TEAL_BF16>(P, stream);
     if (a->w_dtype == TEAL_I8) return launch_w<TEAL_I8>(P, stream);
     return launch_w<TEAL_I4>(P, stream);

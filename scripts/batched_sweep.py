@@ -2,7 +2,8 @@
 int8 / int4 rows at Mistral-7B projection shapes, 50% sparsity (threshold =
 Gaussian quantile of mean |x| over the batch, calibrated per B on the input).
 Reports per-launch time and GB/s on touched weight bytes (kept rows x n x
-bytes-per-element + touched scales).  Rotating weight pool > 2x L2."""
+bytes-per-element + touched scales).  Rotating weight pool > 2x L2; reps launches captured in one CUDA graph
+(device time, CUDA events around the replay)."""
 import argparse
 import json
 import math
@@ -41,13 +42,23 @@ def run(batches=(1, 2, 4, 8, 16), kinds=("bf16", "int8", "int4"), s=0.5, reps=20
                 for i in range(3):
                     Q.sparse_gemv_batched(x, t, pool[i % copies])
                 torch.cuda.synchronize()
+                # device time: the reps launches captured in one CUDA graph (the
+                # ctypes wrapper's host cost per call would otherwise dominate)
+                st = torch.cuda.Stream()
+                st.wait_stream(torch.cuda.current_stream())
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    for i in range(reps):
+                        Q.sparse_gemv_batched(x, t, pool[i % copies])
+                g.replay()
+                torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                for i in range(reps):
-                    Q.sparse_gemv_batched(x, t, pool[i % copies])
+                g.replay()
                 e1.record()
                 torch.cuda.synchronize()
                 us = e0.elapsed_time(e1) * 1e3 / reps
+                del g
                 bpe = {"bf16": 2, "int8": 1, "int4": 0.5}[kind]
                 sc = n * 4 if kind == "int8" else (math.ceil(m / 128) * n * 4 if kind == "int4" else 0)
                 touched = k * n * bpe + sc
