@@ -22,9 +22,9 @@
 // accumulators acc[B][CPL]); warps take kept rows round-robin with U rows in
 // flight; warps are reduced in fixed order, split tiles by the last-arriving
 // CTA in ascending-CTA order (deterministic).  The FMA kernel (CUDA cores)
-// serves int8 / int4 rows and B < 4; bf16 rows at B >= 4 (where the FMA loop
-// is issue-bound, 2*B flops per weight element) run the mma.sync variant
-// below.  At B = 1 the fused single-row kernels are the fast path.
+// serves int4 rows and B < 4; bf16 and int8 rows at B >= 4 (where the FMA
+// loop is issue-bound, 2*B flops per weight element) run the mma.sync
+// variant below.  At B = 1 the fused single-row kernels are the fast path.
 #include "teal_common.cuh"
 #include <string.h>
 
@@ -350,6 +350,7 @@ __device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], 
                  : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+template <int WT>
 __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_constant__ KP P) {
     extern __shared__ __align__(128) unsigned char sm[];
     unsigned char* s_w = sm;                                // [MC][WSTR]
@@ -363,7 +364,10 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_co
     const int c = blockIdx.x;
     const int64_t g0 = (int64_t)c * P.F / P.G, g1 = (int64_t)(c + 1) * P.F / P.G;
     const int B = A.B;
-    const uint16_t* W = reinterpret_cast<const uint16_t*>(A.w);
+    const unsigned char* W = reinterpret_cast<const unsigned char*>(A.w);
+    constexpr int EB = WT == TEAL_I8 ? 1 : 2;          // bytes per weight element
+    constexpr int SEGS = TCM * EB / 16;                // 16-byte requests per row slice
+    constexpr int SOFF = WT == TEAL_I8 ? TCM : 0;      // int8 rows land in the upper half of the slot
     unsigned kcount = 0;
     const int mi = lane >> 3, mr = lane & 7;  // ldmatrix: matrix / row this lane addresses
     for (int64_t gs = g0; gs < g1;) {
@@ -432,15 +436,40 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_co
             __syncthreads();
             if (kpad == 0) continue;  // uniform: nothing kept in this chunk
             // gather the kept rows' tile slices (16 B per request, zero past n)
-            for (int q = tid; q < kpad * (TCM / 8); q += NT) {
-                const int k = q / (TCM / 8), sg = q % (TCM / 8);
-                const int64_t col = tcol0 + sg * 8;
+            for (int q = tid; q < kpad * SEGS; q += NT) {
+                const int k = q / SEGS, sg = q % SEGS;
+                const int64_t col = tcol0 + sg * (16 / EB);
                 const bool inb = col < A.n;
-                const uint16_t* src = W + (int64_t)s_idx[k] * A.ldw + (inb ? col : 0);
-                cp_async16(smem_u32(s_w + k * WSTR + sg * 16), src, inb ? 16 : 0);
+                const unsigned char* src = W + ((int64_t)s_idx[k] * A.ldw + (inb ? col : 0)) * EB;
+                cp_async16(smem_u32(s_w + k * WSTR + SOFF + sg * 16), src, inb ? 16 : 0);
             }
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
             __syncthreads();
+            if constexpr (WT == TEAL_I8) {
+                // widen in place, one half-warp per row: every lane loads its
+                // 16 int8 from the slot's upper half before any lane stores its
+                // 16 bf16 (exact: |q| <= 128) over the row
+                const int c = lane & 15;
+#pragma unroll 1
+                for (int k = warp * 2 + (lane >> 4); k < kpad; k += NW * 2) {
+                    const uint4 q = *reinterpret_cast<const uint4*>(s_w + k * WSTR + TCM + c * 16);
+                    __syncwarp();
+                    const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+                    uint32_t o[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int k0 = 2 * e, k1 = 2 * e + 1;
+                        const float f0 = __uint_as_float(__byte_perm(u[k0 >> 2] ^ 0x80808080u, 0x4B000000u, 0x7540u | (k0 & 3))) - 8388736.0f;
+                        const float f1 = __uint_as_float(__byte_perm(u[k1 >> 2] ^ 0x80808080u, 0x4B000000u, 0x7540u | (k1 & 3))) - 8388736.0f;
+                        o[e] = (__float_as_uint(f0) >> 16) | (__float_as_uint(f1) & 0xffff0000u);
+                    }
+                    uint4* dst = reinterpret_cast<uint4*>(s_w + k * WSTR + c * 32);
+                    dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+                    dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+                    __syncwarp();
+                }
+                __syncthreads();
+            }
             const uint32_t xb = smem_u32(s_xb), wb = smem_u32(s_w);
             const int n0 = warp * 32;
 #pragma unroll 1
@@ -518,7 +547,11 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_co
             for (int q = tid; q < B * TCM; q += NT) {
                 const int b = q / TCM, cc = q - b * TCM;
                 const int64_t col = tcol0 + cc;
-                if (col < A.n) A.y[(int64_t)b * A.n + col] = s_red[b * TCM + cc];
+                if (col < A.n) {
+                    float v = s_red[b * TCM + cc];
+                    if constexpr (WT == TEAL_I8) v *= A.scale[col];
+                    A.y[(int64_t)b * A.n + col] = v;
+                }
             }
         }
         __syncthreads();
@@ -529,7 +562,9 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_co
 // Narrow outputs at B > 8 (few 256-column tiles: many split-K contributors
 // per tile and a long combine) stay on the FMA kernel's 128-column tiles.
 static bool use_mma(const teal_gemv_batched_args* a) {
-    return a->w_dtype == TEAL_BF16 && a->B >= 4 && a->n % 8 == 0 && a->ldw % 8 == 0 && (a->B <= 8 || a->n >= 4096);
+    const bool fmt = (a->w_dtype == TEAL_BF16 && a->n % 8 == 0 && a->ldw % 8 == 0) ||
+                     (a->w_dtype == TEAL_I8 && a->n % 16 == 0 && a->ldw % 16 == 0);
+    return fmt && a->B >= 4 && (a->B <= 8 || a->n >= 4096);
 }
 
 static int cpl_of(int B) { return B > 8 ? 4 : 8; }
@@ -577,6 +612,18 @@ static int validate(const teal_gemv_batched_args* a) {
 }
 
 template <int WT>
+static int launch_mma(const KP& P, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(gemv_batched_mma_kernel<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem) != cudaSuccess)
+            return check_launch("teal_gemv_batched (smem attribute)");
+        attr = true;
+    }
+    gemv_batched_mma_kernel<WT><<<P.G, NT, kMmaSmem, st>>>(P);
+    return check_launch("teal_gemv_batched");
+}
+
+template <int WT>
 static int launch_w(const KP& P, cudaStream_t st) {
     const int bm = bm_of(P.a.B);
     dim3 grid(P.G), block(NT);
@@ -621,16 +668,7 @@ int teal_gemv_batched(const teal_gemv_batched_args* a, cudaStream_t stream) {
     P.a = *a;
     plan(a, &P);
     TEAL_REQUIRE(P.G == 1 || P.maxc == 1 || (a->ws && a->tickets), "teal_gemv_batched: ws and tickets are required");
-    if (use_mma(a)) {
-        static bool attr = false;
-        if (!attr) {
-            if (cudaFuncSetAttribute(gemv_batched_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem) != cudaSuccess)
-                return check_launch("teal_gemv_batched (smem attribute)");
-            attr = true;
-        }
-        gemv_batched_mma_kernel<<<P.G, NT, kMmaSmem, stream>>>(P);
-        return check_launch("teal_gemv_batched");
-    }
+    if (use_mma(a)) return a->w_dtype == TEAL_I8 ? launch_mma<TEAL_I8>(P, stream) : launch_mma<TEAL_BF16>(P, stream);
     if (a->w_dtype == TEAL_BF16) return launch_w<TEAL_BF16>(P, stream);
     if (a->w_dtype == TEAL_I8) return launch_w<TEAL_I8>(P, stream);
     return launch_w<TEAL_I4>(P, stream);

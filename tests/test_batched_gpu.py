@@ -44,6 +44,25 @@ def test_matches_oracle(kind, B):
         assert rel_err(y, ref) < 1e-5, (kind, B, t, rel_err(y, ref))
 
 
+@pytest.mark.parametrize("kind", ["bf16", "int8"])
+@pytest.mark.parametrize("B", [4, 13, 16])
+def test_mma_path_wide_ragged(kind, B):
+    """The tensor-core variant (bf16 / int8 rows, B >= 4; B > 8 only for
+    n >= 4096): ragged m (partial 128-row chunk and 32-row group) and a
+    partial last 256-column tile (n = 4112), against the float64 product of
+    the kernel's own dequantised weights at the fp32 bar (rel 1e-5)."""
+    from paper_2408_14690_b200 import quant as Q
+    m, n = 1000, 4112
+    xs, w = _case(700 + B, B, m, n)
+    qw = {"bf16": Q.as_bf16, "int8": Q.quantize_int8}[kind](torch.from_numpy(w).cuda())
+    wd = qw.dequantize().cpu().numpy().astype(np.float64)
+    for t in (0.0, 0.6745, 1.5):
+        y, mask = Q.sparse_gemv_batched(xs, t, qw, return_mask=True)
+        xs_s, mref = R.sparsify_batched(xs, t)
+        assert np.array_equal(mask, mref), (kind, B, t)
+        assert rel_err(y, xs_s.astype(np.float64) @ wd) < 1e-5, (kind, B, t)
+
+
 def test_dense_and_all_pruned():
     from paper_2408_14690_b200 import quant as Q
     xs, w = _case(7, 4, 512, 256)
