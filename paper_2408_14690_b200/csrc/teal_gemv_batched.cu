@@ -91,6 +91,47 @@ struct KP {
 
 __host__ __device__ __forceinline__ int owner_of(int64_t g, int64_t F, int G) { return (int)(((g + 1) * G - 1) / F); }
 
+
+// Last arriver's split-K combine of one tile: out[q] = sum over contributors
+// k = 0..nc-1 (ascending, from 0.f) of base[k * SLOT + q], q < nout (a
+// multiple of 4).  Each thread owns QPT float4 outputs and, per round, has
+// 4 contributors x QPT float4 loads in flight (clamped indices, masked adds):
+// ceil(nc / 4) L2 round trips instead of one per (output, 16 contributors).
+template <int SLOT>
+__device__ __forceinline__ void combine_tile(const float* base, int nc, int nout, float* out) {
+    constexpr int QPT = (SLOT / 4 + NT - 1) / NT;
+    const int tid = threadIdx.x, nq4 = nout >> 2;
+    const float4* b4 = reinterpret_cast<const float4*>(base);
+    float4 v[QPT];
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k0 = 0; k0 < nc; k0 += 4) {
+        float4 pv[4][QPT];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+            for (int j = 0; j < QPT; ++j) {
+                const int k = min(k0 + kk, nc - 1), q4 = min(tid + j * NT, nq4 - 1);
+                pv[kk][j] = __ldcg(b4 + (int64_t)k * (SLOT / 4) + q4);
+            }
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+            if (k0 + kk < nc)
+#pragma unroll
+                for (int j = 0; j < QPT; ++j) {
+                    v[j].x += pv[kk][j].x;
+                    v[j].y += pv[kk][j].y;
+                    v[j].z += pv[kk][j].z;
+                    v[j].w += pv[kk][j].w;
+                }
+    }
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) {
+        const int q4 = tid + j * NT;
+        if (q4 < nq4) reinterpret_cast<float4*>(out)[q4] = v[j];
+    }
+}
+
 template <int WT, int BM, int CPL>
 __global__ void __launch_bounds__(NT, 2) gemv_batched_kernel(const __grid_constant__ KP P) {
     constexpr int TC = 32 * CPL;
@@ -98,7 +139,7 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_kernel(const __grid_consta
     constexpr int U = 4;
     __shared__ int s_idx[CHUNK];
     __shared__ __align__(16) float s_x[CHUNK * BM];
-    __shared__ float s_red[BM * TC];
+    __shared__ __align__(16) float s_red[BM * TC];
     __shared__ int s_wcnt[NW];
     __shared__ int s_last;
     const teal_gemv_batched_args& A = P.a;
@@ -273,21 +314,7 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_kernel(const __grid_consta
                 // every contributor's partial of this thread's outputs in flight
                 // together (16 at a time, clamped indices), then summed in
                 // ascending contributor order
-                const float* base = A.ws + (int64_t)tile * P.maxc * (BM * TC);
-                const int nc = cl - cf + 1;
-                for (int q = tid; q < BM * TC; q += NT) {
-                    float v = 0.f;
-                    for (int k0 = 0; k0 < nc; k0 += 16) {
-                        float pv[16];
-#pragma unroll
-                        for (int k = 0; k < 16; ++k)
-                            pv[k] = __ldcg(base + (int64_t)(k0 + k < nc ? k0 + k : 0) * (BM * TC) + q);
-#pragma unroll
-                        for (int k = 0; k < 16; ++k)
-                            if (k0 + k < nc) v += pv[k];
-                    }
-                    s_red[q] = v;
-                }
+                combine_tile<BM * TC>(A.ws + (int64_t)tile * P.maxc * (BM * TC), cl - cf + 1, B * TC, s_red);
                 __syncthreads();
             }
         }
@@ -525,21 +552,7 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_co
             __syncthreads();
             fin = *s_last != 0;
             if (fin) {
-                const float* base = A.ws + (int64_t)tile * P.maxc * (16 * TCM);
-                const int nc = cl - cf + 1;
-                for (int q = tid; q < B * TCM; q += NT) {
-                    float v = 0.f;
-                    for (int k0 = 0; k0 < nc; k0 += 16) {
-                        float pv[16];
-#pragma unroll
-                        for (int k = 0; k < 16; ++k)
-                            pv[k] = __ldcg(base + (int64_t)(k0 + k < nc ? k0 + k : 0) * (16 * TCM) + q);
-#pragma unroll
-                        for (int k = 0; k < 16; ++k)
-                            if (k0 + k < nc) v += pv[k];
-                    }
-                    s_red[q] = v;
-                }
+                combine_tile<16 * TCM>(A.ws + (int64_t)tile * P.maxc * (16 * TCM), cl - cf + 1, B * TCM, s_red);
                 __syncthreads();
             }
         }
