@@ -574,10 +574,13 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_co
 
 // Narrow outputs at B > 8 (few 256-column tiles: many split-K contributors
 // per tile and a long combine) stay on the FMA kernel's 128-column tiles.
+#ifndef TEAL_MMA_MIN_B
+#define TEAL_MMA_MIN_B 4
+#endif
 static bool use_mma(const teal_gemv_batched_args* a) {
     const bool fmt = (a->w_dtype == TEAL_BF16 && a->n % 8 == 0 && a->ldw % 8 == 0) ||
                      (a->w_dtype == TEAL_I8 && a->n % 16 == 0 && a->ldw % 16 == 0);
-    return fmt && a->B >= 4 && (a->B <= 8 || a->n >= 4096);
+    return fmt && a->B >= TEAL_MMA_MIN_B;
 }
 
 static int cpl_of(int B) { return B > 8 ? 4 : 8; }
