@@ -22,9 +22,9 @@
 // accumulators acc[B][CPL]); warps take kept rows round-robin with U rows in
 // flight; warps are reduced in fixed order, split tiles by the last-arriving
 // CTA in ascending-CTA order (deterministic).  The FMA kernel (CUDA cores)
-// serves int4 rows and B < 4; bf16 and int8 rows at B >= 4 (where the FMA
-// loop is issue-bound, 2*B flops per weight element) run the mma.sync
-// variant below.  At B = 1 the fused single-row kernels are the fast path.
+// serves B < 4; bf16 / int8 / int4 (group % 128 == 0) rows at B >= 4 (where
+// the FMA loop is issue-bound, 2*B flops per weight element) run the
+// mma.sync variant below.  At B = 1 the fused single-row kernels are the fast path.
 #include "teal_common.cuh"
 #include <string.h>
 
@@ -392,9 +392,12 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_co
     const int64_t g0 = (int64_t)c * P.F / P.G, g1 = (int64_t)(c + 1) * P.F / P.G;
     const int B = A.B;
     const unsigned char* W = reinterpret_cast<const unsigned char*>(A.w);
-    constexpr int EB = WT == TEAL_I8 ? 1 : 2;          // bytes per weight element
-    constexpr int SEGS = TCM * EB / 16;                // 16-byte requests per row slice
-    constexpr int SOFF = WT == TEAL_I8 ? TCM : 0;      // int8 rows land in the upper half of the slot
+    // bytes of one row slice; int8 / int4 slices land at the end of the
+    // slot (upper half / last quarter) and are widened to bf16 in place
+    constexpr int RB = WT == TEAL_I8 ? TCM : (WT == TEAL_I4 ? TCM / 2 : TCM * 2);
+    constexpr int SEGS = RB / 16;                      // 16-byte requests per row slice
+    constexpr int EPS = TCM / SEGS;                    // elements per request
+    constexpr int SOFF = 2 * TCM - RB;
     unsigned kcount = 0;
     const int mi = lane >> 3, mr = lane & 7;  // ldmatrix: matrix / row this lane addresses
     for (int64_t gs = g0; gs < g1;) {
@@ -409,8 +412,15 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_co
         for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[j][q] = 0.f;
-        for (int ra = r0; ra < r1; ra += MC) {
-            const int rb = min(r1, ra + MC);
+        float gtot[4][4];  // int4: scaled sum over the chunks (one row group each)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) gtot[j][q] = 0.f;
+        // chunks end at multiples of MC, so with group % MC == 0 a chunk lies
+        // inside one int4 scale group
+        for (int ra = r0, rb; ra < r1; ra = rb) {
+            rb = min(r1, (ra / MC + 1) * MC);
             // shared mask of the chunk (threads 0..MC-1 own one row each)
             const int i = ra + tid;
             const bool v = tid < MC && i < rb;
@@ -465,9 +475,9 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_co
             // gather the kept rows' tile slices (16 B per request, zero past n)
             for (int q = tid; q < kpad * SEGS; q += NT) {
                 const int k = q / SEGS, sg = q % SEGS;
-                const int64_t col = tcol0 + sg * (16 / EB);
+                const int64_t col = tcol0 + sg * EPS;
                 const bool inb = col < A.n;
-                const unsigned char* src = W + ((int64_t)s_idx[k] * A.ldw + (inb ? col : 0)) * EB;
+                const unsigned char* src = W + ((int64_t)s_idx[k] * A.ldw + (inb ? col : 0)) * RB / TCM;
                 cp_async16(smem_u32(s_w + k * WSTR + SOFF + sg * 16), src, inb ? 16 : 0);
             }
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
@@ -497,6 +507,43 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_co
                 }
                 __syncthreads();
             }
+            if constexpr (WT == TEAL_I4) {
+                // widen in place, one quarter-warp per row (32 nibbles per
+                // lane, low nibble = even column; exact in bf16)
+                const int c = lane & 7;
+#pragma unroll 1
+                for (int kb = warp * 4; kb < kpad; kb += NW * 4) {  // kpad % 4 == 0: uniform per warp
+                    const int k = kb + (lane >> 3);
+                    const uint4 q = *reinterpret_cast<const uint4*>(s_w + k * WSTR + SOFF + c * 16);
+                    __syncwarp();
+                    const uint32_t u[4] = {q.x ^ 0x88888888u, q.y ^ 0x88888888u, q.z ^ 0x88888888u, q.w ^ 0x88888888u};
+                    uint4* dst = reinterpret_cast<uint4*>(s_w + k * WSTR + c * 64);
+#pragma unroll
+                    for (int v4 = 0; v4 < 4; ++v4) {
+                        uint32_t o[4];
+#pragma unroll
+                        for (int e2 = 0; e2 < 4; ++e2) {
+                            const int e0 = v4 * 8 + e2 * 2, e1 = e0 + 1;
+                            const float f0 = __uint_as_float(((u[e0 >> 3] >> (4 * (e0 & 7))) & 0xfu) | 0x4B000000u) - 8388616.0f;
+                            const float f1 = __uint_as_float(((u[e1 >> 3] >> (4 * (e1 & 7))) & 0xfu) | 0x4B000000u) - 8388616.0f;
+                            o[e2] = (__float_as_uint(f0) >> 16) | (__float_as_uint(f1) & 0xffff0000u);
+                        }
+                        dst[v4] = make_uint4(o[0], o[1], o[2], o[3]);
+                    }
+                    __syncwarp();
+                }
+                __syncthreads();
+            }
+            float2 gsc[4];  // int4: this chunk's group scales of the thread's 8 columns
+            if constexpr (WT == TEAL_I4) {
+                const int64_t grow = (int64_t)(ra / A.group) * A.n;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int64_t col = tcol0 + warp * 32 + j * 8 + 2 * (lane & 3);
+                    gsc[j] = __ldg(reinterpret_cast<const float2*>(A.scale + grow + (col < A.n ? col : 0)));
+                    if (col >= A.n) gsc[j] = make_float2(0.f, 0.f);
+                }
+            }
             const uint32_t xb = smem_u32(s_xb), wb = smem_u32(s_w);
             const int n0 = warp * 32;
 #pragma unroll 1
@@ -517,7 +564,24 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_co
                     }
                 }
             }
+            if constexpr (WT == TEAL_I4) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    gtot[j][0] = fmaf(acc[j][0], gsc[j].x, gtot[j][0]);
+                    gtot[j][1] = fmaf(acc[j][1], gsc[j].y, gtot[j][1]);
+                    gtot[j][2] = fmaf(acc[j][2], gsc[j].x, gtot[j][2]);
+                    gtot[j][3] = fmaf(acc[j][3], gsc[j].y, gtot[j][3]);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[j][q] = 0.f;
+                }
+            }
             __syncthreads();  // the stage is rewritten by the next chunk
+        }
+        if constexpr (WT == TEAL_I4) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[j][q] = gtot[j][q];
         }
         // warp-owned columns: D fragment -> s_red[b][col] (no cross-warp sum)
         {
@@ -579,7 +643,8 @@ __global__ void __launch_bounds__(NT, 2) gemv_batched_mma_kernel(const __grid_co
 #endif
 static bool use_mma(const teal_gemv_batched_args* a) {
     const bool fmt = (a->w_dtype == TEAL_BF16 && a->n % 8 == 0 && a->ldw % 8 == 0) ||
-                     (a->w_dtype == TEAL_I8 && a->n % 16 == 0 && a->ldw % 16 == 0);
+                     (a->w_dtype == TEAL_I8 && a->n % 16 == 0 && a->ldw % 16 == 0) ||
+                     (a->w_dtype == TEAL_I4 && a->n % 32 == 0 && a->ldw % 32 == 0 && a->group % MC == 0);
     return fmt && a->B >= TEAL_MMA_MIN_B;
 }
 
@@ -684,7 +749,9 @@ int teal_gemv_batched(const teal_gemv_batched_args* a, cudaStream_t stream) {
     P.a = *a;
     plan(a, &P);
     TEAL_REQUIRE(P.G == 1 || P.maxc == 1 || (a->ws && a->tickets), "teal_gemv_batched: ws and tickets are required");
-    if (use_mma(a)) return a->w_dtype == TEAL_I8 ? launch_mma<TEAL_I8>(P, stream) : launch_mma<TEAL_BF16>(P, stream);
+    if (use_mma(a))
+        return a->w_dtype == TEAL_I8 ? launch_mma<TEAL_I8>(P, stream)
+             : a->w_dtype == TEAL_I4 ? launch_mma<TEAL_I4>(P, stream) : launch_mma<TEAL_BF16>(P, stream);
     if (a->w_dtype == TEAL_BF16) return launch_w<TEAL_BF16>(P, stream);
     if (a->w_dtype == TEAL_I8) return launch_w<TEAL_I8>(P, stream);
     return launch_w<TEAL_I4>(P, stream);

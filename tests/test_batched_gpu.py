@@ -44,17 +44,19 @@ def test_matches_oracle(kind, B):
         assert rel_err(y, ref) < 1e-5, (kind, B, t, rel_err(y, ref))
 
 
-@pytest.mark.parametrize("kind", ["bf16", "int8"])
+@pytest.mark.parametrize("kind", ["bf16", "int8", "int4"])
 @pytest.mark.parametrize("B", [4, 13, 16])
 def test_mma_path_wide_ragged(kind, B):
-    """The tensor-core variant (bf16 / int8 rows, B >= 4; B > 8 only for
-    n >= 4096): ragged m (partial 128-row chunk and 32-row group) and a
-    partial last 256-column tile (n = 4112), against the float64 product of
-    the kernel's own dequantised weights at the fp32 bar (rel 1e-5)."""
+    """The tensor-core variant (bf16 / int8 / int4-group-128 rows, B >= 4):
+    ragged m (partial 128-row chunk, 32-row group and int4 scale group) and
+    a partial last 256-column tile (n = 4112; 4128 for int4, whose MMA path
+    needs n % 32 == 0), against the float64 product of the kernel's own
+    dequantised weights at the fp32 bar (rel 1e-5)."""
     from paper_2408_14690_b200 import quant as Q
-    m, n = 1000, 4112
+    m, n = 1000, (4128 if kind == "int4" else 4112)
     xs, w = _case(700 + B, B, m, n)
-    qw = {"bf16": Q.as_bf16, "int8": Q.quantize_int8}[kind](torch.from_numpy(w).cuda())
+    qw = {"bf16": Q.as_bf16, "int8": Q.quantize_int8,
+          "int4": lambda a: Q.quantize_int4(a, 128)}[kind](torch.from_numpy(w).cuda())
     wd = qw.dequantize().cpu().numpy().astype(np.float64)
     for t in (0.0, 0.6745, 1.5):
         y, mask = Q.sparse_gemv_batched(xs, t, qw, return_mask=True)
