@@ -466,6 +466,13 @@ def run_ours(args):
         del W
         torch.cuda.empty_cache()
         sweep["gemv_gbs"] = gemv_sweep([0.0, 0.4, 0.5])
+        # config 5: Mistral-7B gate shape, batched shared-mask GEMV at 50 %
+        # (device time of graph-captured launches; scripts/batched_sweep.py)
+        sys.path.insert(0, str(ROOT / "scripts"))
+        import batched_sweep
+        rows = batched_sweep.run(batches=(1, 4, 16), shapes={"gate": batched_sweep.SHAPES["gate"]}, quiet=True)
+        sweep["batched_gate_50"] = {f'{r["kind"]}_B{r["B"]}': {"us": r["us"], "gbs": r["gbs"], "tflops": round(r["gflops"] / 1e3, 2)}
+                                    for r in rows}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:

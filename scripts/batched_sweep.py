@@ -18,7 +18,7 @@ from paper_2408_14690_b200 import quant as Q  # noqa: E402
 SHAPES = {"q": (4096, 4096), "kv": (1024, 4096), "o": (4096, 4096), "gate": (14336, 4096), "down": (4096, 14336)}
 
 
-def run(batches=(1, 2, 4, 8, 16), kinds=("bf16", "int8", "int4"), s=0.5, reps=20, shapes=SHAPES):
+def run(batches=(1, 2, 4, 8, 16), kinds=("bf16", "int8", "int4"), s=0.5, reps=20, shapes=SHAPES, quiet=False):
     dev = torch.device("cuda")
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     out = []
@@ -66,7 +66,8 @@ def run(batches=(1, 2, 4, 8, 16), kinds=("bf16", "int8", "int4"), s=0.5, reps=20
                        "gbs": round(touched / (us * 1e-6) / 1e9, 1),
                        "gflops": round(2 * B * k * n / (us * 1e-6) / 1e9, 1)}
                 out.append(row)
-                print(json.dumps(row), flush=True)
+                if not quiet:
+                    print(json.dumps(row), flush=True)
             del pool
         del w
         torch.cuda.empty_cache()
