@@ -694,11 +694,15 @@ static int validate(const teal_gemv_batched_args* a) {
 
 template <int WT>
 static int launch_mma(const KP& P, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    // the dynamic shared memory opt-in is per device
+    static unsigned long long done = 0ull;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return check_launch("teal_gemv_batched (device)");
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(__atomic_load_n(&done, __ATOMIC_ACQUIRE) & bit)) {
         if (cudaFuncSetAttribute(gemv_batched_mma_kernel<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem) != cudaSuccess)
             return check_launch("teal_gemv_batched (smem attribute)");
-        attr = true;
+        __atomic_fetch_or(&done, bit, __ATOMIC_RELEASE);
     }
     gemv_batched_mma_kernel<WT><<<P.G, NT, kMmaSmem, st>>>(P);
     return check_launch("teal_gemv_batched");
