@@ -101,6 +101,17 @@ def sparse_gemv_batched(xs, t: float, w: QuantWeights, return_mask: bool = False
     if m != w.m:
         raise ValueError(f"dimension mismatch: x rows have length {m}, W has {w.m} input channels")
     dev = x.device
+    t32 = float("-inf") if t is None or t == float("-inf") else RT.f32_round_nearest(float(t))
+    if B == 1 and not return_mask and w.dtype in (C.TEAL_BF16, C.TEAL_I8) and w.data.dtype in (torch.bfloat16, torch.int8):
+        # one row: mean_b |x| = |x| exactly, so the shared mask is sparsify's
+        # fp32 `|x| <= fl32(t)` — the single-row split-K kernel (the fast B = 1
+        # path) with that threshold gives the same mask and kept count
+        y1 = torch.empty(w.n, device=dev)
+        a1 = RT.single_gemv_args(w.data, w.n, x[0], t32, y1, w.scale if w.dtype == C.TEAL_I8 else None, kept)
+        RT.bind_workspace(a1, dev)
+        RT.launch_gemv(a1)
+        y = y1.view(1, w.n)
+        return y.cpu().numpy() if host else y
     y = torch.empty(B, w.n, device=dev)
     mask = torch.empty(m, dtype=torch.uint8, device=dev) if return_mask else None
     a = C.TealGemvBatchedArgs()
@@ -108,7 +119,7 @@ def sparse_gemv_batched(xs, t: float, w: QuantWeights, return_mask: bool = False
     a.mask, a.kept = RT.ptr(mask), RT.ptr(kept)
     a.m, a.n, a.ldw = m, w.n, w.n
     a.w_dtype, a.group, a.B = w.dtype, w.group, B
-    a.t32 = float("-inf") if t is None or t == float("-inf") else RT.f32_round_nearest(float(t))
+    a.t32 = t32
     g, nws, ntk = ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
     C.call("teal_gemv_batched_workspace", ctypes.byref(a), ctypes.byref(g), ctypes.byref(nws), ctypes.byref(ntk))
     ws, tk = RT.workspace(nws.value, ntk.value, dev)

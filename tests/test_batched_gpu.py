@@ -84,6 +84,25 @@ def test_batch1_equals_single_row_sparsify():
     assert np.array_equal(~mask, R.keep_mask(xs[0], 0.5))
 
 
+@pytest.mark.parametrize("kind", ["bf16", "int8"])
+def test_batch1_single_row_route(kind):
+    """B = 1 without a mask request runs the single-row kernel: same kept
+    count as the batched kernel (mask identical by construction) and the
+    same product at the fp32 bar."""
+    from paper_2408_14690_b200 import quant as Q
+    xs, w = _case(31, 1, 1536, 1280)
+    qw = {"bf16": Q.as_bf16, "int8": Q.quantize_int8}[kind](torch.from_numpy(w).cuda())
+    wd = qw.dequantize().cpu().numpy().astype(np.float64)
+    for t in (0.0, 0.6745, 2.0):
+        k1 = torch.zeros(1, dtype=torch.int64, device="cuda")
+        y = Q.sparse_gemv_batched(xs, t, qw, kept=k1)
+        yb, mask = Q.sparse_gemv_batched(xs, t, qw, return_mask=True)
+        xs_s, mref = R.sparsify_batched(xs, t)
+        assert int(k1.item()) == int((~mref).sum()), (kind, t)
+        assert rel_err(y, xs_s.astype(np.float64) @ wd) < 1e-5, (kind, t)
+        assert rel_err(y, yb) < 1e-5, (kind, t)
+
+
 def test_golden_batched_masks():
     # masks of the real reference's sparsify_batched on seeds 40000+s
     from paper_2408_14690_b200 import quant as Q
