@@ -12,6 +12,8 @@ quantised weights).
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import pytest
 import torch
@@ -63,6 +65,27 @@ def test_mma_path_wide_ragged(kind, B):
         xs_s, mref = R.sparsify_batched(xs, t)
         assert np.array_equal(mask, mref), (kind, B, t)
         assert rel_err(y, xs_s.astype(np.float64) @ wd) < 1e-5, (kind, B, t)
+
+
+@pytest.mark.parametrize("kind", ["bf16", "int8", "int4"])
+def test_config5_full_shape(kind):
+    """BASELINE config 5 at its real size: Mistral-7B gate 4096 x 14336,
+    B = 16, threshold at the 50 % quantile of the batch-mean magnitude.
+    Mask bit-exact against the oracle's sparsify_batched; product against a
+    float64 product of the dequantised weights (on the device) at rel 1e-5."""
+    from paper_2408_14690_b200 import quant as Q
+    m, n, B = 4096, 14336, 16
+    g = torch.Generator(device="cuda").manual_seed(55)
+    x = torch.randn(B, m, device="cuda", generator=g)
+    w = torch.randn(m, n, device="cuda", generator=g) / math.sqrt(m)
+    qw = {"bf16": Q.as_bf16, "int8": Q.quantize_int8, "int4": lambda a: Q.quantize_int4(a, 128)}[kind](w)
+    t = float(torch.quantile(x.abs().mean(0), 0.5))
+    y, mask = Q.sparse_gemv_batched(x, t, qw, return_mask=True)
+    xs_s, mref = R.sparsify_batched(x.cpu().numpy(), t)
+    assert np.array_equal(mask.cpu().numpy(), mref)
+    assert 0.45 < float(mref.mean()) < 0.55
+    ref = torch.from_numpy(xs_s).cuda().double() @ qw.dequantize().double()
+    assert rel_err(y.cpu().numpy(), ref.cpu().numpy()) < 1e-5, kind
 
 
 def test_dense_and_all_pruned():
