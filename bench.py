@@ -272,13 +272,24 @@ def make_decoder(engine, W, thr, count_kept=False):
     return D.SparseDecoder(W, thr)
 
 
-def decode_tok_s(D, W, thr, steps, warmup, ws, engine="step"):
+def decode_tok_s(D, W, thr, steps, warmup, ws, engine="step", gbs_out=None):
+    """tok/s of `steps` replays; with gbs_out (a dict) and the step engine,
+    also the step's algorithmic GB/s (kept channels counted on the device
+    during the timed steps), stored under gbs_out["gbs"]."""
     import torch
-    dec = make_decoder(engine, W, thr)
+    count = gbs_out is not None and engine == "step"
+    dec = make_decoder(engine, W, thr, count_kept=count)
     capture_steps(dec)
     for _ in range(warmup):
         dec.replay()
+    torch.cuda.synchronize()
+    if count:
+        dec.kept.zero_()
+        pos0 = int(dec.state[1].item())
     ms = timed(dec.replay, steps, ws)
+    if count:
+        positions = sum(pos0 + i + 1 for i in range(steps))
+        gbs_out["gbs"] = dec.algorithmic_bytes(dec.kept, steps=steps, positions=positions) / (ms * 1e-3) / 1e9
     n = dec.launches_per_step()
     del dec
     torch.cuda.empty_cache()
@@ -449,11 +460,16 @@ def run_ours(args):
     sweep = None
     if not args.no_sweep:
         n_sw = max(20, args.steps // 2)
-        dense_tok, _, _ = decode_tok_s(D, W, None, n_sw, 3, ws, args.engine)
+        gd = {}
+        dense_tok, _, _ = decode_tok_s(D, W, None, n_sw, 3, ws, args.engine, gbs_out=gd)
         dec_rows = {"dense": round(dense_tok, 2)}
+        frac_rows = {"dense": round(gd["gbs"] / peak, 3)} if "gbs" in gd else {}
         for s in levels:
-            tok, _, _ = decode_tok_s(D, W, thr[s], n_sw, 3, ws, args.engine)
+            gl = {}
+            tok, _, _ = decode_tok_s(D, W, thr[s], n_sw, 3, ws, args.engine, gbs_out=gl)
             dec_rows[str(s)] = round(tok, 2)
+            if "gbs" in gl:
+                frac_rows[str(s)] = round(gl["gbs"] / peak, 3)
         other = "launch" if args.engine == "step" else "step"
         other_rows = {"dense": round(decode_tok_s(D, W, None, n_sw, 3, ws, other)[0], 2),
                       str(args.sparsity): round(decode_tok_s(D, W, thr[args.sparsity], n_sw, 3, ws, other)[0], 2)}
@@ -462,7 +478,8 @@ def run_ours(args):
                  "speedup_vs_dense": {k: round(v / dense_tok, 3) for k, v in dec_rows.items() if k != "dense"},
                  f"{other}_engine_tok_s": other_rows,
                  "dense_weight_gb_per_token": round(wb / 1e9, 3),
-                 "dense_hbm_frac": round(dense_tok * wb / 1e9 / peak, 3)}
+                 "dense_hbm_frac": round(dense_tok * wb / 1e9 / peak, 3),
+                 "hbm_roofline_frac": frac_rows}
         del W
         torch.cuda.empty_cache()
         sweep["gemv_gbs"] = gemv_sweep([0.0, 0.4, 0.5])
