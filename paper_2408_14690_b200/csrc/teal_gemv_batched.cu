@@ -661,7 +661,11 @@ static int plan(const teal_gemv_batched_args* a, KP* P) {
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
         sms = 148;
     cudaGetLastError();
-    int64_t G = a->ctas > 0 ? a->ctas : 2LL * sms;
+    // MMA variant over few column tiles (k/v: n = 1024, 4 tiles): one CTA per
+    // SM halves the split-K contributors per tile (k/v B = 16 19 -> 16 us);
+    // wider outputs keep two resident CTAs to overlap their chunk chains
+    const bool narrow = use_mma(a) && P->ntiles <= 4;
+    int64_t G = a->ctas > 0 ? a->ctas : (narrow ? 1LL : 2LL) * sms;
     if (G > P->F) G = P->F;
     P->G = (int)G;
     int maxc = 1;
