@@ -399,7 +399,7 @@ typedef struct teal_step_plan {
     unsigned long long* timeline;    /* nullable debug: [ctas][nphases][8] %globaltimer */
     int nphases, ncounters;
     int prefetch_bytes;              /* per CTA per GEMV phase: L2 prefetch of its weight range head (0: off) */
-    int pad_;
+    int max_seq;                     /* KV-cache positions: LOAD traps when len >= max_seq (0: unchecked) */
     int d, emb_dtype;
     int w_dtype, ctas;               /* ctas: grid size (<= resident capacity)  */
     long long* acc_zero;             /* LOAD: ACC accumulators zeroed each step */

@@ -151,6 +151,9 @@ __device__ __forceinline__ void run_epilogue(const KParams& P, int seg, int tis,
         __syncthreads();
         const int hd = A.head_dim, half = hd >> 1;
         const int pos = *A.pos;
+        // a position past the cache would write into the next head's / layer's
+        // slice (and read RoPE tables out of bounds): fail loudly instead
+        if (pos < 0 || pos >= A.max_seq) asm volatile("trap;");
         const bool rope = (A.rope_cos != nullptr) && (seg < 2);
 #pragma unroll
         for (int q = 0; q < QN; ++q) {

@@ -1500,6 +1500,10 @@ __device__ __noinline__ void load_phase(const teal_step_plan& P) {
     }
     if (tid == 0) {
         const int len = P.state[1];
+        // the step writes K/V row `len`: past max_seq it would land in the next
+        // head's / layer's cache slice — fail loudly (the engines also check
+        // on the host; inside a graph replay only this guard can)
+        if (len < 0 || (P.max_seq > 0 && len >= P.max_seq)) asm volatile("trap;");
         P.state[0] = len;
         P.state[1] = len + 1;
     }

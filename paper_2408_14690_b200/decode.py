@@ -236,6 +236,7 @@ class SparseDecoder:
             self.taps.kept = torch.zeros(L, 7, device=dev, dtype=torch.int64)
         self._build(thresholds)
         self.graph = None
+        self._pos = 0
 
     # -- launch descriptors ---------------------------------------------------
     def _build(self, thresholds):
@@ -332,9 +333,18 @@ class SparseDecoder:
     def reset(self, start_pos: int = 0) -> None:
         """Forget the cache; the next step writes position `start_pos`."""
         self.state.copy_(torch.tensor([start_pos - 1, start_pos], dtype=torch.int32))
+        self._pos = start_pos
         if start_pos == 0:
             self.kcache.zero_()
             self.vcache.zero_()
+
+    def _advance(self) -> None:
+        """Host-side position guard: the step about to run writes K/V row
+        `_pos`, which must lie inside the cache (the QKV epilogue also traps)."""
+        if self._pos >= self.spec.max_seq:
+            raise ValueError(f"decode position {self._pos} would exceed max_seq {self.spec.max_seq} "
+                             f"(the KV cache holds positions [0, {self.spec.max_seq}))")
+        self._pos += 1
 
     def launches_per_step(self) -> int:
         return 1 + 5 * self.spec.n_layers + (2 if self.lm_args is not None else 0)
@@ -371,12 +381,14 @@ class SparseDecoder:
             self.x_in.copy_(x_row.reshape(-1), non_blocking=True)
         else:
             self.x_in.copy_(torch.from_numpy(np.ascontiguousarray(x_row, dtype=np.float32)), non_blocking=True)
+        self._advance()
         self._launch_step(RT.stream_handle(), from_token=False)
         return self.x
 
     def step_token(self) -> torch.Tensor:
         """One step from self.token (embedding lookup); leaves the argmax next
         token in self.token and returns it."""
+        self._advance()
         if self.graph is not None:
             self.graph.replay()
         else:
@@ -404,6 +416,7 @@ class SparseDecoder:
         return g
 
     def replay(self) -> None:
+        self._advance()
         self.graph.replay()
 
 

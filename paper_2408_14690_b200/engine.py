@@ -69,7 +69,7 @@ class StepPlan(ctypes.Structure):
     _fields_ = [("groups", c_vp), ("attns", c_vp), ("phases", c_vp), ("counters", c_vp), ("ctrl", c_vp),
                 ("emb", c_vp), ("x_in", c_vp), ("token", c_vp), ("x", c_vp), ("ss", c_vp), ("state", c_vp),
                 ("cand_v", c_vp), ("cand_i", c_vp), ("token_out", c_vp), ("lm_done", c_vp), ("timeline", c_vp),
-                ("nphases", c_i), ("ncounters", c_i), ("prefetch_bytes", c_i), ("pad_", c_i),
+                ("nphases", c_i), ("ncounters", c_i), ("prefetch_bytes", c_i), ("max_seq", c_i),
                 ("d", c_i), ("emb_dtype", c_i), ("w_dtype", c_i), ("ctas", c_i),
                 ("acc_zero", c_vp), ("acc_zero_n", c_i64), ("tp", c_vp), ("noncoop", c_i), ("long_ctx", c_i),
                 ("phase_begin", c_i), ("phase_end", c_i)]
@@ -428,6 +428,7 @@ class StepDecoder:
         self.super_chunks = int(long_context) if long_context and long_context > 1 else 1
         self.long_from = int(long_from)
         self._pos = 0
+        self.last_long = False  # which kernel variant the latest step ran
         self.graph_long = None
         self.nchunks = -(-spec.max_seq // attn_chunk)
         self.taps = StepTaps() if taps else None
@@ -663,6 +664,7 @@ class StepDecoder:
         p.w_dtype, p.ctas = self.w_code, self.grid
         p.long_ctx = 0  # chosen per launch (_use_long)
         p.prefetch_bytes = self.prefetch_bytes
+        p.max_seq = spec.max_seq
         self.plan = p
 
     def _upload_plan(self) -> None:
@@ -747,6 +749,11 @@ class StepDecoder:
     def _use_long(self) -> bool:
         return self.super_chunks > 1 and self._pos >= self.long_from
 
+    def _check_pos(self) -> None:
+        if self._pos >= self.spec.max_seq:
+            raise ValueError(f"decode position {self._pos} would exceed max_seq {self.spec.max_seq} "
+                             f"(the KV cache holds positions [0, {self.spec.max_seq}))")
+
     def _launch(self, stream_h: int, from_token: bool, long_ctx: bool | None = None) -> None:
         p = self.plan
         p.long_ctx = int(self._use_long() if long_ctx is None else long_ctx)
@@ -761,7 +768,9 @@ class StepDecoder:
             self.x_in.copy_(x_row.reshape(-1), non_blocking=True)
         else:
             self.x_in.copy_(torch.from_numpy(np.ascontiguousarray(x_row, dtype=np.float32)), non_blocking=True)
+        self._check_pos()
         self._launch(RT.stream_handle(), from_token=False)
+        self.last_long = bool(self.plan.long_ctx)
         self._pos += 1
         return self.x
 
@@ -769,7 +778,9 @@ class StepDecoder:
         if self.graph is not None:
             self.replay()
         else:
+            self._check_pos()
             self._launch(RT.stream_handle(), from_token=True)
+            self.last_long = bool(self.plan.long_ctx)
             self._pos += 1
         return self.token
 
@@ -796,5 +807,7 @@ class StepDecoder:
         return self.graph
 
     def replay(self) -> None:
-        (self.graph_long if self._use_long() and self.graph_long is not None else self.graph).replay()
+        self._check_pos()
+        self.last_long = self._use_long() and self.graph_long is not None
+        (self.graph_long if self.last_long else self.graph).replay()
         self._pos += 1

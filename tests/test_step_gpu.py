@@ -245,3 +245,28 @@ def test_long_context_switches_by_position():
             dec.step_token()
             torch.cuda.synchronize()
             assert rel_err(dec.x.cpu().numpy(), ref[i][0].cpu().numpy()) < 1e-3, (graph, i)
+            assert dec.last_long == (i >= 30), (graph, i)  # the variant that actually ran
+
+
+@pytest.mark.parametrize("engine", ["step", "launch"])
+@pytest.mark.parametrize("graph", [False, True])
+def test_position_past_max_seq_raises(engine, graph):
+    # the KV cache holds max_seq positions: the step that would write row
+    # max_seq is refused on the host (the kernels also trap on it)
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200 import engine as E
+    spec = D.DecoderSpec(1024, 8, 2, 2816, 1, vocab=1000, rope_theta=500000.0, norm_eps=1e-5, max_seq=4)
+    W = D.random_weights(spec, torch.bfloat16, seed=3)
+    dec = E.StepDecoder(W, None) if engine == "step" else D.SparseDecoder(W, None)
+    dec.reset()
+    if graph:
+        dec.capture()
+        dec.reset()
+    for _ in range(4):
+        dec.step_token()
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError, match="max_seq"):
+        dec.step_token()
+    dec.reset(start_pos=3)
+    dec.step_token()
+    torch.cuda.synchronize()
