@@ -352,7 +352,9 @@ typedef struct teal_step_attn {
     int nq, nkv;             /* q / k columns (qkv_acc offsets)               */
     int super_chunks;        /* long-context kernel (plan.long_ctx): one unit walks this
                                 many chunks with an online softmax (>= 1)           */
-    int pad_;
+    int home;                /* > 0: CTAs [home, grid) take no part in the qkv phase; when
+                                the units fit there, unit u runs on CTA home + u (it stages
+                                its K/V rows while qkv streams and waits ready) */
 } teal_step_attn;
 
 typedef struct teal_step_phase {

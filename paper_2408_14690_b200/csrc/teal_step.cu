@@ -815,12 +815,13 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
     // into L2 (one bulk prefetch of contiguous tiled rows): the wait is tail
     // time of the previous phase, when HBM is mostly idle.  Rows that turn out
     // pruned cost idle bandwidth only; kept rows then stream from L2.
-    if (tid == 0 && P.prefetch_bytes > 0) {
+    const int pf_bytes = P.prefetch_bytes;
+    if (tid == 0 && pf_bytes > 0) {
         const int tile = tile_of(g0, gpt);
         const int r0 = (int)(g0 - (int64_t)tile * gpt) * 32;
         const int r1 = min(g.m, (int)(min64(g1, (int64_t)(tile + 1) * gpt) - (int64_t)tile * gpt) * 32);
         const int64_t rowb = WFmt<WT>::ROWB;
-        const int64_t bytes = min64((int64_t)(r1 - r0) * rowb, (int64_t)P.prefetch_bytes) & ~(int64_t)15;
+        const int64_t bytes = min64((int64_t)(r1 - r0) * rowb, (int64_t)pf_bytes) & ~(int64_t)15;
         if (bytes > 0) {
             const unsigned char* src = reinterpret_cast<const unsigned char*>(g.w) + ((int64_t)tile * g.m + r0) * rowb;
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((uint32_t)bytes) : "memory");
@@ -835,11 +836,13 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
         if (P.tp) wait_range_sys(P.counters, ph.dep, ph.dep, ph.target);
         else wait_range(P.counters, ph.dep, ph.dep, ph.target);
     }
+    if (tl && tid == 0) tl[6] = gtimer();  // global dependency met
     // PRO_RMSNORM: rden computed by the first compaction, overlapped with its x loads
     float rden = rms ? -1.f : 1.f;
     if (racc) {
         if (g.xwait < 0) rms_stage_x(g, s);
         rden = rms_acc_finish(g, c, G, s);
+        if (tl && tid == 0) tl[7] = gtimer();  // RMS prologue done
         if (g.xsig >= 0) signal(P.counters, g.xsig, g.xsig);  // x_out share written
     }
     constexpr int ROWB = WFmt<WT>::ROWB;
@@ -943,8 +946,7 @@ __device__ void gemv_slice_t(const teal_step_plan& P, const teal_step_phase& ph,
         ++lasts;
         if (segi == 0) SL_STAMP(4, gtimer());
     }
-    SL_STAMP(6, (unsigned long long)segi);
-    SL_STAMP(7, (unsigned long long)lasts);
+    (void)lasts;
 #undef SL_STAMP
 }
 
@@ -1078,12 +1080,15 @@ __device__ __noinline__ void attn_unit(const teal_step_plan& P, const teal_step_
     float* my = a.partials + ((int64_t)g * a.nchunks + ch) * rec;
     const int64_t kvbase = (int64_t)g * a.max_seq * hd;
     unsigned long long* dbg = a.dbg ? a.dbg + ((int64_t)g * a.nchunks + ch) * 6 : nullptr;
-#define ATT_STAMP(k) do { if (dbg && tid == 0) dbg[k] = gtimer(); } while (0)
+    // stamps 0, 1: %globaltimer (ns); 2..5: SM clock cycles since stamp 1
+    long long ck1 = 0;
+#define ATT_STAMP(k) do { if (dbg && tid == 0) { if ((k) < 2) { dbg[k] = gtimer(); ck1 = clock64(); } else dbg[k] = (unsigned long long)(clock64() - ck1); } } while (0)
     ATT_STAMP(0);
     const int pos = L - 1;
     const int newrow = (a.qkv_acc && pos >= p0 && pos < p1) ? pos - p0 : -1;
     if (np > 0) attn_stage_kv(a, p0, np, newrow, kvbase);
     wait_range(P.counters, a.dep_base + g, a.dep_base + g, a.dep_target[g]);  // q / new row ready
+    ATT_STAMP(1);
     if (np > 0) {
         attn_stage_q(a, g, pos, newrow, kvbase);
         __syncthreads();
@@ -1126,7 +1131,7 @@ __device__ __noinline__ void attn_unit(const teal_step_plan& P, const teal_step_
             s.u.a.sc[h * ATT_MAXCHUNK + p] = ((acc4.x + acc4.y) + (acc4.z + acc4.w)) * rs;
         }
         __syncthreads();
-        ATT_STAMP(1);
+        ATT_STAMP(3);
         // softmax statistics: warp per head
 #pragma unroll 1
         for (int h = warp; h < G; h += NW) {
@@ -1205,7 +1210,6 @@ __device__ __noinline__ void attn_unit(const teal_step_plan& P, const teal_step_
             }
         }
         if (single) {
-            ATT_STAMP(3);
             ATT_STAMP(4);
             signal(P.counters, a.sig_base + g, a.sig_base + g);
             ATT_STAMP(5);
@@ -1219,11 +1223,9 @@ __device__ __noinline__ void attn_unit(const teal_step_plan& P, const teal_step_
         __stcg(my + G * hd + tid, -INFINITY);
         __stcg(my + G * hd + G + tid, 0.f);
     }
-    ATT_STAMP(2);
     // only the chunks holding positions take part (the attn phase skips the rest)
     const int nact = min(a.nchunks, (L + a.chunk - 1) / a.chunk);
     const bool last = take_ticket(a.tickets + g, (unsigned)nact - 1u, s.last);
-    ATT_STAMP(3);
     if (!last) return;
     const float* rb = a.partials + (int64_t)g * a.nchunks * rec;
     for (int q = tid; q < nact * 2 * G; q += NT) {  // (m, l) of every active chunk -> smem
@@ -1448,7 +1450,18 @@ __device__ void attn_phase(const teal_step_plan& P, const teal_step_phase& ph, S
     const int nact = min(a.nchunks, (L + a.chunk - 1) / a.chunk);  // chunks holding positions
     const int nu = LC ? a.KVH * ((nact + a.super_chunks - 1) / a.super_chunks) : a.KVH * nact;
     const int G = gridDim.x;
-    // unit u = (chunk u / KVH, kv group u % KVH) runs on CTA G-1 - (u*G)/nu:
+    // the units fit on the CTAs the qkv phase leaves idle: unit u on CTA home + u
+    // (they stage their K/V rows while qkv streams and poll from the start)
+    if (a.home > 0 && nu <= G - a.home) {
+        const int u = (int)blockIdx.x - a.home;
+        if (u >= 0 && u < nu) {
+            const int g = u % a.KVH, ch = u / a.KVH;
+            if constexpr (LC) attn_unit_multi(P, a, g, ch, L);
+            else attn_unit(P, a, g, ch, L);
+        }
+        return;
+    }
+    // otherwise unit u = (chunk u / KVH, kv group u % KVH) runs on CTA G-1 - (u*G)/nu:
     // spread over the grid from its end (the qkv phase leaves the last CTAs idle)
     const int cr = G - 1 - (int)blockIdx.x;
     for (int u = (int)(((int64_t)cr * nu + G - 1) / G); u < nu && (int64_t)u * G / nu == cr; ++u) {

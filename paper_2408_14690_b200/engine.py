@@ -58,7 +58,7 @@ class StepAttn(ctypes.Structure):
                 ("tickets", c_vp), ("max_seq", c_i64), ("H", c_i), ("KVH", c_i), ("hd", c_i), ("kv_dtype", c_i),
                 ("chunk", c_i), ("nchunks", c_i), ("sig_base", c_i), ("dep_base", c_i), ("dep_target", c_vp),
                 ("dbg", c_vp), ("qkv_acc", c_vp), ("rope_cos", c_vp), ("rope_sin", c_vp), ("nq", c_i), ("nkv", c_i),
-                ("super_chunks", c_i), ("pad_", c_i)]
+                ("super_chunks", c_i), ("home", c_i)]
 
 
 class StepPhase(ctypes.Structure):
@@ -640,6 +640,10 @@ class StepDecoder:
         if spec.vocab:
             gl = groups[4 * L]
             gl.xwait, gl.xwait_target = cbase(L - 1)["xg"], ctas_of(groups[4 * (L - 1) + 2])
+        # attention units on the CTAs the qkv phase leaves idle (when they fit)
+        for l in range(L):
+            pq = ctas_of(groups[4 * l])
+            attns[l].home = pq if Gc - pq >= KVH else 0
         self._keep = keep
         self._groups_host = (StepGroup * len(groups))(*groups)
         self._phases_host = (StepPhase * len(phases))(*phases)
@@ -676,8 +680,10 @@ class StepDecoder:
         """Debug: record %globaltimer at entry/exit of every phase of every CTA
         ([grid, nphases, 8] int64, overwritten by each launch): 0 start, 1 end;
         GEMV phases also 2 prologue done (first segment's rows ready), 3/5
-        first/second segment streamed, 4 first segment finished, 6 segments,
-        7 global dependency met."""
+        first/second segment streamed, 4 first segment finished, 6 global
+        dependency met, 7 RMS prologue done (RMS_ACC phases).  Attention
+        units (attn_debug): 0 entry, 1 q/k/v tiles ready, 2 q staged,
+        3 scores, 4 context written, 5 signalled."""
         self.timeline = torch.zeros(self.grid, self.nphases, 8, device=self.device, dtype=torch.int64)
         self.plan.timeline = self.timeline.data_ptr()
         return self.timeline

@@ -64,6 +64,9 @@ for _ in range(a.steps):
             d.setdefault("ready", []).append(torch.quantile(rd, qs) / 1e3)
             d.setdefault("strm", []).append(torch.quantile(s3, qs) / 1e3)
             d.setdefault("strm_dur", []).append(torch.quantile(s3 - rd, qs) / 1e3)
+            if nm in ("qkv", "gu"):
+                d.setdefault("dep_met", []).append(torch.quantile(t[act, p, 6] - T0, qs) / 1e3)
+                d.setdefault("rms_done", []).append(torch.quantile(t[act, p, 7] - T0, qs) / 1e3)
         d.setdefault("end", []).append(torch.quantile(en, qs) / 1e3)
 print(f"s={a.s} layers {a.l0}..{a.l1 - 1} of {spec.n_layers}, {a.steps} steps; us relative to previous phase's last end")
 print(f"{'':12s} {'p10':>7s} {'p50':>7s} {'p90':>7s} {'max':>7s}")
@@ -73,22 +76,28 @@ for nm in ("qkv", "attn", "o", "gu", "down"):
         m = torch.stack(v).mean(0)
         print(f"  {k:10s} " + " ".join(f"{float(x):7.2f}" for x in m))
 
-# attention units: internal stamps (attn_debug) relative to the qkv phase's last end
+# attention units: internal stamps (attn_debug) of the LAST layer relative to
+# its qkv phase's last end, averaged over steps
 dec2 = E.StepDecoder(W, thr, attn_debug=True)
 dec2.reset()
 for _ in range(a.warm):
     dec2.step_token()
 tl2 = dec2.enable_timeline()
-dec2.step_token()
-torch.cuda.synchronize()
-t = tl2.cpu().double()
-ad = dec2.attn_dbg.cpu().double()
-print("attention units of the LAST layer (stamps: 0 entry, 2 q staged, 1 scores, 3 ctx, 5 signalled), us vs qkv last end")
 p_qkv = 1 + 5 * (spec.n_layers - 1)
-T0 = t[:, p_qkv, 1].max()
-qkv_end_by_cta = t[:, p_qkv, 1]
-for u in range(ad.shape[0]):
-    r = ad[u]
-    if r[0] <= 0:
-        continue
-    print("  unit", u, " ".join(f"{k}:{(float(r[k]) - float(T0)) / 1e3:6.2f}" for k in (0, 2, 1, 3, 5)))
+acc = []
+for _ in range(a.steps):
+    dec2.step_token()
+    torch.cuda.synchronize()
+    t = tl2.cpu().double()
+    ad = dec2.attn_dbg.cpu().double()
+    T0 = t[:, p_qkv, 1].max()
+    act = ad[:, 0] > 0
+    r = ad[act].clone()
+    r[:, :2] = (r[:, :2] - T0) / 1e3          # us vs the qkv phase's last end
+    r[:, 2:] = r[:, 2:] / 1965.0               # SM cycles since 'tiles ready' -> us at 1965 MHz
+    acc.append(r)
+m = torch.stack(acc).mean(0)
+print("attention units, last layer: entry / tiles ready (us vs qkv last end); then us after tiles ready: "
+      "q staged, scores, ctx, signalled")
+for u in range(m.shape[0]):
+    print("  unit", u, " ".join(f"{k}:{float(m[u, k]):6.2f}" for k in range(6)))
