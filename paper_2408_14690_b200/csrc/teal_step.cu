@@ -999,19 +999,28 @@ __device__ __noinline__ void attn_stage_kv(const teal_step_attn& a, int p0, int 
 __device__ __noinline__ void attn_stage_q(const teal_step_attn& a, int g, int pos, int newrow, int64_t kvbase) {
     Smem& s = smem();
     constexpr int QPT = ATT_MAXG * ATT_MAXHD / NT;
+    // the fields, read once: the struct lives in global memory, and a store
+    // through one of its pointers would make the compiler re-read the next
+    // field it needs after that store (a dependent global load per store)
+    const long long* const qkv_acc = a.qkv_acc;
+    const float* const rope_cos = a.rope_cos;
+    const float* const rope_sin = a.rope_sin;
+    void* const k_cache = const_cast<void*>(a.k_cache);
+    void* const v_cache = const_cast<void*>(a.v_cache);
+    const int kv_dtype = a.kv_dtype, nq = a.nq, nkv = a.nkv;
     const int tid = threadIdx.x, G = a.H / a.KVH, hd = a.hd, half = hd >> 1;
-    const bool acc = a.qkv_acc != nullptr;
+    const bool acc = qkv_acc != nullptr;
     // NT is a multiple of hd: every element this thread touches (q heads and
     // the new k) has head dim d = tid % hd, so one RoPE pair serves all
     const int d = tid % hd, dd = d < half ? d : d - half;
     const int part = d < half ? half : -half;
-    const bool rope = acc && a.rope_cos;
+    const bool rope = acc && rope_cos;
     long long qa[QPT], qp[QPT], ka = 0, kp = 0, va = 0;
     float qf[QPT];
     float cs = 1.f, sn = 0.f;
     if (rope) {
-        cs = __ldg(a.rope_cos + (int64_t)pos * half + dd);
-        sn = __ldg(a.rope_sin + (int64_t)pos * half + dd);
+        cs = __ldg(rope_cos + (int64_t)pos * half + dd);
+        sn = __ldg(rope_sin + (int64_t)pos * half + dd);
     }
     // straight-line loads (clamped indices; unused values are never consumed)
     const bool nk = newrow >= 0 && tid < hd;
@@ -1020,14 +1029,14 @@ __device__ __noinline__ void attn_stage_q(const teal_step_attn& a, int g, int po
         for (int j = 0; j < QPT; ++j) {
             const int o = tid + j * NT;
             const int64_t qc = (int64_t)g * G * hd + (o < G * hd ? o : d);
-            qa[j] = __ldcg(a.qkv_acc + qc);
-            qp[j] = __ldcg(a.qkv_acc + qc + part);
+            qa[j] = __ldcg(qkv_acc + qc);
+            qp[j] = __ldcg(qkv_acc + qc + part);
             qf[j] = 0.f;
         }
-        const int64_t kc = (int64_t)a.nq + (int64_t)g * hd + d;
-        ka = __ldcg(a.qkv_acc + kc);
-        kp = __ldcg(a.qkv_acc + kc + part);
-        va = __ldcg(a.qkv_acc + kc + a.nkv);
+        const int64_t kc = (int64_t)nq + (int64_t)g * hd + d;
+        ka = __ldcg(qkv_acc + kc);
+        kp = __ldcg(qkv_acc + kc + part);
+        va = __ldcg(qkv_acc + kc + nkv);
     } else {
 #pragma unroll
         for (int j = 0; j < QPT; ++j) {
@@ -1050,16 +1059,16 @@ __device__ __noinline__ void attn_stage_q(const teal_step_attn& a, int g, int po
         float kr = rope ? fmaf(sgn * from_fx(kp), sn, from_fx(ka) * cs) : from_fx(ka);
         float vr = from_fx(va);
         const int64_t off = kvbase + (int64_t)pos * hd + d;
-        if (a.kv_dtype == TEAL_BF16) {
+        if (kv_dtype == TEAL_BF16) {
             const uint16_t kb = f32_to_bf16_rn(kr), vb = f32_to_bf16_rn(vr);
-            reinterpret_cast<uint16_t*>(const_cast<void*>(a.k_cache))[off] = kb;
-            reinterpret_cast<uint16_t*>(const_cast<void*>(a.v_cache))[off] = vb;
+            __stcg(reinterpret_cast<unsigned short*>(k_cache) + off, kb);
+            __stcg(reinterpret_cast<unsigned short*>(v_cache) + off, vb);
         } else {
-            reinterpret_cast<float*>(const_cast<void*>(a.k_cache))[off] = kr;
-            reinterpret_cast<float*>(const_cast<void*>(a.v_cache))[off] = vr;
+            __stcg(reinterpret_cast<float*>(k_cache) + off, kr);
+            __stcg(reinterpret_cast<float*>(v_cache) + off, vr);
         }
-        const int vpr = hd * (a.kv_dtype == TEAL_BF16 ? 2 : 4) / 16;
-        if (a.kv_dtype == TEAL_BF16) {
+        const int vpr = hd * (kv_dtype == TEAL_BF16 ? 2 : 4) / 16;
+        if (kv_dtype == TEAL_BF16) {
             reinterpret_cast<uint16_t*>(s.u.a.k + newrow * (vpr + 1))[d] = f32_to_bf16_rn(kr);
             reinterpret_cast<uint16_t*>(s.u.a.v)[newrow * hd + d] = f32_to_bf16_rn(vr);
         } else {
