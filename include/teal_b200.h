@@ -5,7 +5,18 @@
  * cudaStream_t, returns an int status (TEAL_OK = 0) and never allocates,
  * frees or synchronises.  The last error message of the calling thread is
  * available from teal_last_error().  No C++ exception crosses this boundary.
- * All launches are stream-ordered and CUDA-graph capturable.
+ * All launches are stream-ordered and CUDA-graph capturable.  The library
+ * reads no environment variables; its only process-wide state is a per-
+ * process cache of immutable device facts (SM count, kernel occupancy) and
+ * of one-time kernel attributes (dynamic shared-memory opt-in), all
+ * idempotent.
+ *
+ * teal_sparse_gemv / teal_dense_gemv / teal_fused_gemv calls with one
+ * segment, the PLAIN prologue, the STORE epilogue, fp32 x and bf16 / fp32 /
+ * int8 rows run on the persistent step kernel's streaming core
+ * (gemv_one_kernel in teal_step.cu, split tiles combined in contributor
+ * order); every other fused variant runs the gemv_tma / register kernels of
+ * teal_gemv.cu.  Both paths have the same masks and MAC counts.
  *
  * Reference interfaces replaced (paths relative to the reference tree):
  *   teal_threshold         <- sparsifier.sparsify / realized_sparsity
@@ -44,6 +55,7 @@ extern "C" {
 /* element types */
 #define TEAL_F32 0
 #define TEAL_BF16 1
+#define TEAL_F64 4      /* teal_hist_record input only (the reference bins float64) */
 #define TEAL_I8 2       /* int8 rows, per-output-column fp32 scale */
 #define TEAL_I4 3       /* int4 rows (two per byte, low nibble = even column),
                            fp32 scale per (group of input rows, column) */
@@ -184,7 +196,9 @@ int teal_gemv_batched(const teal_gemv_batched_args* a, cudaStream_t stream);
 
 /* counts[b] += #{i : floor(|x_i|/hi*bins) clipped to bins-1 == b, |x_i| <= hi}
  * overflow  += #{i : |x_i| > hi};  nan_flag set to 1 if any NaN.
- * Binning in fp64 exactly as numpy (sparsifier.py:75-80). */
+ * Binning in fp64 exactly as numpy (sparsifier.py:75-80); x_dtype TEAL_F32,
+ * TEAL_BF16 or TEAL_F64 (float64 input is binned unrounded, as the reference
+ * does with np.asarray(x, float64)). */
 int teal_hist_record(const void* x, int x_dtype, int64_t count, double hi, int bins,
                      unsigned long long* counts, unsigned long long* overflow,
                      unsigned int* nan_flag, cudaStream_t stream);
@@ -242,10 +256,14 @@ int teal_argmax(const float* logits, int64_t n, int* out_token,
  * into tiles of TEAL_STEP_TW columns and tile t is the contiguous block
  * w[t][i][0..TW) over input channels i (element (out t*TW + c, in i) =
  * w[(t*m + i)*TW + c]); a kept channel streams one contiguous row chunk per
- * tile, fetched by the TMA engine (cp.async.bulk) into a per-warp shared
- * memory ring.  Each tile carries two column halves with their own
- * thresholds (gate | up interleaved for the MLP).  A tile split across CTAs
- * is finished by its last-arriving contributor, summing the fp32 partials in
+ * tile, register-streamed by the warps (16-byte non-allocating loads, L2
+ * evict-first, the next rows' loads in flight while the current ones are
+ * consumed).  Each tile carries two column halves with their own thresholds
+ * (gate | up interleaved for the MLP).  Layer outputs are int64 fixed-point
+ * accumulators (ACC, 2^-32 units) that every contributor of a tile adds its
+ * column partials into with red.add — integer addition is associative, so
+ * the result does not depend on arrival order; the LM head's split tiles are
+ * finished by their last-arriving contributor, summing fp32 partials in
  * contributor order (deterministic two-phase reduction). */
 #define TEAL_STEP_TW 256
 #define TEAL_PHASE_LOAD 0

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "lib" / "libteal_b200.so"
 
 TEAL_OK, TEAL_EINVAL, TEAL_ECUDA = 0, 1, 2
-TEAL_F32, TEAL_BF16, TEAL_I8, TEAL_I4 = 0, 1, 2, 3
+TEAL_F32, TEAL_BF16, TEAL_I8, TEAL_I4, TEAL_F64 = 0, 1, 2, 3, 4
 PRO_PLAIN, PRO_RMSNORM = 0, 1
 EPI_STORE, EPI_RESID, EPI_SILU, EPI_QKV = 0, 1, 2, 3
 

@@ -17,6 +17,7 @@ from . import _clib as C
 
 _ws_lock = threading.Lock()
 _ws_cache: dict = {}
+_ws_retired: list = []  # grown-out-of workspaces (CUDA graphs may still point at them)
 
 
 def require_cuda() -> torch.device:
@@ -44,6 +45,8 @@ def dtype_code(dt: torch.dtype) -> int:
         return C.TEAL_BF16
     if dt == torch.int8:
         return C.TEAL_I8
+    if dt == torch.float64:
+        return C.TEAL_F64
     raise ValueError(f"unsupported dtype {dt}")
 
 
@@ -56,9 +59,15 @@ def workspace(nfloats: int, ntickets: int, device=None, stream: torch.cuda.Strea
     key = (dev.index if dev.index is not None else torch.cuda.current_device(), stream_handle(stream))
     with _ws_lock:
         ws, tk = _ws_cache.get(key, (None, None))
+        # superseded buffers stay alive: a CUDA graph captured over an earlier
+        # call keeps their raw pointers
         if ws is None or ws.numel() < nfloats:
+            if ws is not None:
+                _ws_retired.append(ws)
             ws = torch.empty(max(nfloats, 1 << 16), dtype=torch.float32, device=dev)
         if tk is None or tk.numel() < ntickets:
+            if tk is not None:
+                _ws_retired.append(tk)
             tk = torch.zeros(max(ntickets, 4096), dtype=torch.int32, device=dev)
         _ws_cache[key] = (ws, tk)
     return ws, tk

@@ -51,7 +51,7 @@ struct KParams {
     int ns;         // bulk-copy ring slots (TMA path)
     int emax;       // smem entry-list capacity per CTA
     int ntmax;      // max tiles per CTA range
-    int timeline;   // TEAL_TIMELINE=1: record per-CTA phase timestamps
+    int timeline;   // debug builds: record per-CTA phase timestamps
 };
 
 // Phase timeline probe (debug): g_teal_tl[cta*4 + k] = %globaltimer at
@@ -721,23 +721,12 @@ static bool seg_wide_ok(const teal_gemv_args* a) {
     return true;
 }
 
-int pdl_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TEAL_PDL");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v;
-}
+// Programmatic dependent launch between consecutive GEMV launches (the next
+// launch's prologue overlaps this one's tail): always on.
+int pdl_enabled() { return 1; }
 
-static int slot_kb() {
-    static int kb = 0;
-    if (!kb) {
-        const char* e = getenv("TEAL_SLOT_KB");
-        kb = (e && atoi(e) == 2) ? 2 : 1;
-    }
-    return kb;
-}
+// 1 KB bulk-copy slots per row segment (TmaCfg::NS = 64 slots)
+static int slot_kb() { return 1; }
 
 static int tile_width(const teal_gemv_args* a) {
     const int esz = esz_of(a->w_dtype);
@@ -771,11 +760,7 @@ static int plan(const teal_gemv_args* a, KParams* P) {
     P->gpt = (int)((a->m + 31) / 32);
     P->F = (int64_t)t * P->gpt;
     int64_t G = a->ctas;
-    if (G <= 0) {
-        int per_sm = 2;
-        if (const char* e = getenv("TEAL_CTAS_PER_SM")) per_sm = atoi(e) > 0 ? atoi(e) : 2;
-        G = (int64_t)sm_count_cached() * per_sm;
-    }
+    if (G <= 0) G = (int64_t)sm_count_cached() * 2;  // 2 resident CTAs per SM
     if (G > P->F) G = P->F;
     if ((P->F + 1) * G >= (int64_t)1 << 32) G = ((int64_t)1 << 32) / (P->F + 1) - 1;  // keep index math 32-bit
     // a range must not span more than NT_MAX tiles
@@ -788,8 +773,7 @@ static int plan(const teal_gemv_args* a, KParams* P) {
     P->emax = (int)(per * 32);
     P->maxc = (int)((P->gpt * G + P->F - 1) / P->F + 1);
     P->ns = 64 / slot_kb();  // TMA ring slots (TmaCfg::NS)
-    const char* tl = getenv("TEAL_TIMELINE");
-    P->timeline = (tl && tl[0] == '1') ? 1 : 0;
+    P->timeline = 0;  // (debug probe: set to 1 in a build to record phase stamps)
     return TEAL_OK;
 }
 
@@ -937,8 +921,11 @@ int teal_fused_gemv(const teal_gemv_args* a, cudaStream_t stream) {
         TEAL_REQUIRE(P.tile % a->head_dim == 0 && a->seg[0].n % a->head_dim == 0 && a->seg[1].n % a->head_dim == 0,
                      "teal_fused_gemv: QKV epilogue needs head_dim | tile (%d) and head_dim | n", P.tile);
     TEAL_REQUIRE(a->ws && a->tickets, "teal_fused_gemv: ws and tickets are required");
-    // plain single-projection calls run on the persistent step kernel's streaming core
-    if (getenv("TEAL_OLD_GEMV") == nullptr && teal::step_gemv_eligible(a, nullptr, nullptr, nullptr) == 0)
+    // Plain single-projection calls (one segment, PLAIN prologue, STORE
+    // epilogue, fp32 x, bf16/fp32/int8 rows) run on the persistent step
+    // kernel's streaming core (gemv_one_kernel, teal_step.cu), documented in
+    // include/teal_b200.h; the fused prologue/epilogue variants run here.
+    if (teal::step_gemv_eligible(a, nullptr, nullptr, nullptr) == 0)
         return teal::step_gemv_single(a, stream);
     const bool xb = (a->x_dtype == TEAL_BF16);
     if (a->w_dtype == TEAL_BF16) return xb ? launch<uint16_t, uint16_t>(P, stream) : launch<uint16_t, float>(P, stream);

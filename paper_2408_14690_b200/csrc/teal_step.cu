@@ -12,10 +12,11 @@
 //   * GEMV phase: the flattened (column tile, 32-channel group) space is cut
 //     into G equal contiguous ranges, CTA c owning [c*F/G, (c+1)*F/G) — equal
 //     input channels to threshold and, in expectation, equal kept rows to
-//     stream, so CTAs finish a phase together.  A range spans a few tiles;
-//     a tile shared by several CTAs is finished by its last-arriving
-//     contributor (ticket), which sums the fp32 partials in contributor order
-//     (deterministic two-phase reduction) and runs the fused epilogue.
+//     stream, so CTAs finish a phase together.  A range spans one or two
+//     tiles; layer outputs are int64 fixed-point accumulators every
+//     contributor adds into (the consumer applies the epilogue while loading
+//     its input); the LM head's split tiles are finished by the last-arriving
+//     contributor (ticket), summing fp32 partials in contributor order.
 //   * Dependencies are counters bumped (release) by tile epilogues and
 //     polled (acquire) before a slice reads its input rows: o waits only for
 //     the attention groups its rows come from, down only for the gate/up
@@ -30,11 +31,16 @@
 //      sum of sum-of-squares partials); keep_lo/hi = !(|h_i| <= t_lo/hi)
 //      (closed prune boundary, NaN kept); ordered CTA-local compaction with
 //      warp ballot/popc;
-//   2. warp w takes kept rows w, w+8, ...; its lane 0 keeps S row chunks in
-//      flight with cp.async.bulk (TMA engine, L2 evict-first) into the warp's
-//      private shared-memory ring (one mbarrier per slot, only the kept
-//      halves are copied); lanes read 16 B each and FMA into fp32 registers;
-//   3. fixed-order cross-warp reduction -> TW column sums.
+//   2. warp w takes kept rows w*U.., w*U + NW*U.., register-streamed: each
+//      lane issues 16-byte (bf16/fp32), 8-byte (int8) or 4-byte (int4)
+//      ld.global.nc.L1::no_allocate loads with an L2 evict-first policy, the
+//      next U rows' loads in flight before the current U are consumed; only
+//      the kept half of a row is loaded; fp32 FMA into per-lane registers;
+//   3. fixed-order cross-warp reduction -> TW column sums, then either an
+//      int64 fixed-point red.add into the tile's accumulator (ACC outputs:
+//      order-independent, so deterministic, and nobody waits) or, for the
+//      LM head, fp32 partials summed in contributor order by the tile's last
+//      arriving contributor (ticket).
 // No tensor cores: a batch-1 matvec is ~1 flop/byte.
 #include "teal_common.cuh"
 #include <string.h>
@@ -1617,24 +1623,14 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const __grid_constant__ 
     }
 }
 
-// Kernel variant: default 2 CTAs/SM with 6 rows per pipeline stage (128
-// registers; measured on the 8B step: UB 5 / 6 / 7 / 8 / 10 -> 370 / 413 /
-// 410 / 406 / 361 tok/s at 50%); TEAL_STEP_OCC=3 selects 3 CTAs/SM with 4
-// rows per stage (80 registers; measured slower: spills).
-static int occ_mode() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TEAL_STEP_OCC");
-        v = (e && e[0] == '3') ? 3 : 2;
-    }
-    return v;
-}
-
+// Kernel variants: 2 CTAs/SM with 6 rows per pipeline stage (128 registers;
+// measured on the 8B step: UB 5 / 6 / 7 / 8 / 10 -> 370 / 413 / 410 / 406 /
+// 361 tok/s at 50%; 3 CTAs/SM with 4 rows per stage spilled and was slower),
+// and the long-context attention variant of the same configuration.
 template <int WT>
 static void* kernel_ptr_t(bool lc) {
     if (lc) return (void*)step_kernel<WT, 2, 6, true>;
-    if (occ_mode() == 2) return (void*)step_kernel<WT, 2, 6>;
-    return (void*)step_kernel<WT, 3, 4>;
+    return (void*)step_kernel<WT, 2, 6>;
 }
 
 static void* kernel_ptr(int w_dtype, bool lc = false) {

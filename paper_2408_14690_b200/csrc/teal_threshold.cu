@@ -52,6 +52,12 @@ __global__ void __launch_bounds__(kThreads) threshold_batched_kernel(const float
 // Histogram of |x| on [0, hi] in fp64: idx = floor(|x| / hi * bins), clipped to
 // the last bin, |x| > hi -> overflow.  Shared-memory privatised 32-bit bins,
 // flushed with 64-bit global atomics (integer, so order-independent).
+// the value binned: fp64 input as is (the reference bins np.asarray(x,
+// float64), sparsifier.py:75-80), fp32 / bf16 widened exactly
+__device__ __forceinline__ double hist_value(double v) { return v; }
+__device__ __forceinline__ double hist_value(float v) { return (double)v; }
+__device__ __forceinline__ double hist_value(uint16_t v) { return (double)bf16_to_f32(v); }
+
 template <typename XT>
 __global__ void __launch_bounds__(kThreads) hist_kernel(const XT* __restrict__ x, int64_t cnt, double hi, int bins,
                                                         unsigned long long* __restrict__ counts,
@@ -66,7 +72,7 @@ __global__ void __launch_bounds__(kThreads) hist_kernel(const XT* __restrict__ x
     unsigned ov = 0;
     bool nan = false;
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * kThreads) {
-        const double v = fabs((double)to_f32<XT>(x[i]));
+        const double v = fabs(hist_value(x[i]));
         if (isnan(v)) {
             nan = true;
         } else if (v > hi) {
@@ -200,12 +206,15 @@ int teal_hist_record(const void* x, int x_dtype, int64_t count, double hi, int b
     if (use_smem && smem > 48 * 1024) {
         cudaFuncSetAttribute(hist_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(hist_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(hist_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     const int g = grid_for(count, kThreads * 16, 148 * 4);
     if (x_dtype == TEAL_F32)
         hist_kernel<float><<<g, kThreads, smem, stream>>>((const float*)x, count, hi, bins, counts, overflow, nan_flag, use_smem);
     else if (x_dtype == TEAL_BF16)
         hist_kernel<uint16_t><<<g, kThreads, smem, stream>>>((const uint16_t*)x, count, hi, bins, counts, overflow, nan_flag, use_smem);
+    else if (x_dtype == TEAL_F64)
+        hist_kernel<double><<<g, kThreads, smem, stream>>>((const double*)x, count, hi, bins, counts, overflow, nan_flag, use_smem);
     else
         TEAL_REQUIRE(false, "teal_hist_record: unsupported dtype %d", x_dtype);
     return check_launch("teal_hist_record");

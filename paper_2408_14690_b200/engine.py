@@ -361,7 +361,7 @@ class StepDecoder:
 
     def __init__(self, weights, thresholds=None, kv_dtype=None, device=None,
                  taps: bool = False, attn_chunk: int = 0, ctas: int = 0,
-                 count_kept: bool = False, attn_debug: bool = False, prefetch_kb: int | None = None,
+                 count_kept: bool = False, attn_debug: bool = False, prefetch_kb: int = 0,
                  quant: str | None = None, long_context: int = 0, long_from: int = 2048):
         self.w = weights
         spec = self.spec = weights.spec
@@ -441,9 +441,6 @@ class StepDecoder:
         # kept-channel counters accumulated over every step (for algorithmic bytes)
         self.kept = self.taps.kept if taps else (torch.zeros(L, 7, device=dev, dtype=torch.int64) if count_kept else None)
         self.ctas = ctas
-        if prefetch_kb is None:
-            import os
-            prefetch_kb = int(os.environ.get("TEAL_STEP_PREFETCH_KB", "0"))
         self.prefetch_bytes = max(0, int(prefetch_kb)) * 1024
         self.attn_dbg = torch.zeros(spec.n_kv_heads * self.nchunks, 6, device=dev, dtype=torch.int64) if attn_debug else None
         self._build(thresholds)
@@ -607,8 +604,7 @@ class StepDecoder:
             self.cand_i = torch.zeros(1, device=dev, dtype=torch.int32)
         self.lm_done = torch.zeros(1, device=dev, dtype=torch.int32)
         # ACC groups whose equal split crosses tiles (gate/up): weighted ranges
-        import os
-        pen = int(os.environ.get("TEAL_SEG_PENALTY", "10"))  # measured: 0 -> 31.7 us, 10 -> 29.5 us gate/up
+        pen = 10  # groups charged for a second segment; measured: 0 -> 31.7 us, 10 -> 29.5 us gate/up
         self.range_tables = {}
         for gi, g in enumerate(groups):
             if not g.acc or g.m <= 0:

@@ -43,6 +43,19 @@ def _device_input(x):
     return torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).to(dev), a.shape, True
 
 
+def _hist_input(x):
+    """Flat CUDA tensor for histogram binning: float64 stays float64 (host
+    arrays are uploaded unrounded), fp32 / bf16 as they are."""
+    if isinstance(x, torch.Tensor):
+        if x.dtype == torch.float64:
+            return x.to(RT.require_cuda() if not x.is_cuda else x.device).contiguous().reshape(-1)
+        return _device_input(x)[0]
+    a = np.asarray(x)
+    if a.dtype == np.float64:
+        return torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).to(RT.require_cuda())
+    return _device_input(x)[0]
+
+
 def threshold_bits(x, t: float):
     """(keep bitmask uint32 words, pruned count tensor) for a CUDA vector —
     bit i%32 of word i//32 is set iff !(|x_i| <= fl32(t))."""
@@ -74,8 +87,11 @@ def realized_sparsity(x, t: float) -> float:
     xd, _, _ = _device_input(x)
     if xd.numel() == 0:
         raise ValueError("realized sparsity of an empty vector is undefined")
+    t32 = RT.f32_round_nearest(t)
+    if not t32 >= 0.0:  # no validation in the reference: |x| <= t holds nowhere
+        return 0.0
     pruned = torch.zeros(1, dtype=torch.int64, device=xd.device)
-    C.call("teal_threshold", RT.ptr(xd), RT.dtype_code(xd.dtype), xd.numel(), RT.f32_round_nearest(t),
+    C.call("teal_threshold", RT.ptr(xd), RT.dtype_code(xd.dtype), xd.numel(), t32,
            None, None, RT.ptr(pruned), RT.stream_handle())
     return float(int(pruned.item())) / xd.numel()
 
@@ -163,8 +179,10 @@ class ActivationHistogram:
 
     def record(self, x) -> "ActivationHistogram":
         """Add |x_i| for every entry of x; values above hi count as overflow.
-        NaN input raises ValueError and leaves the histogram unchanged."""
-        xd, _, _ = _device_input(x)
+        NaN input raises ValueError and leaves the histogram unchanged.
+        float64 input is binned at float64 (the reference's np.asarray(x,
+        float64), sparsifier.py:75-80), everything else at its own precision."""
+        xd = _hist_input(x)
         n = xd.numel()
         if n == 0:
             return self

@@ -48,6 +48,9 @@ class TestSparsify:
 
     def test_realized_boundary_and_empty(self, T):
         assert T.realized_sparsity([1.0, 2.0, 3.0], 3.0) == 1.0
+        # the reference does not validate t: a negative or NaN t prunes nothing
+        for t in (-0.5, float("nan")):
+            assert T.realized_sparsity([0.0, -0.5, 2.0], t) == R.realized_sparsity([0.0, -0.5, 2.0], t) == 0.0
         assert T.realized_sparsity([0.1, -0.5, 2.0, -0.05], 0.2) == 0.5
         with pytest.raises(ValueError):
             T.realized_sparsity([], 0.1)
@@ -141,6 +144,23 @@ class TestHistogram:
         h = T.ActivationHistogram.empty("t", 4, 1.0)
         h.record(np.array([0.5, 2.0, 1.0], dtype=np.float32))
         assert h.overflow_count == 1 and h.total == 3 and h.counts.sum() == 2
+
+    def test_float64_input_binned_unrounded(self, T):
+        # values within fp32 rounding of bin edges and of hi: the reference
+        # bins np.asarray(x, float64) (sparsifier.py:75-80) — an fp32 upload
+        # would move them across edges
+        bins, hi = 1000, 1.0
+        edges = np.arange(1, bins, dtype=np.float64) / bins
+        xs = np.concatenate([edges - 1e-12, edges + 1e-12, [hi, hi + 1e-12, hi - 1e-12], -edges[:50] - 1e-13])
+        h = T.ActivationHistogram.empty("f64", bins, hi)
+        h.record(xs)
+        cnt, ov = np.zeros(bins, np.int64), 0
+        cnt, ov = R.hist_record(cnt, ov, xs, hi)
+        assert np.array_equal(h.counts, cnt) and h.overflow_count == ov and h.total == xs.size
+        import torch
+        h2 = T.ActivationHistogram.empty("f64d", bins, hi)
+        h2.record(torch.from_numpy(xs).cuda())
+        assert np.array_equal(h2.counts, cnt) and h2.overflow_count == ov
 
     def test_nan_rejected_without_mutation(self, T):
         h = T.ActivationHistogram.empty("t", 4, 1.0)
