@@ -58,6 +58,13 @@ sys.path.insert(0, str(ROOT))
 METRIC = "batch-1 decode tokens/sec & sparse-GEMV HBM GB/s at 0/40/50% sparsity"
 UNIT = "tokens/s"
 FALLBACK_HBM_GBS = 6650.0
+# Why the timed CPU path is the port: the reference is Python + numba
+# (no C/C++ to compile into oracle/_ref), /root/reference does not exist on
+# the GPU box and this tier ships nothing of it, so its own `sparse_gemv`
+# cannot run here; the port is bit-identical to it (tests/test_oracle_golden)
+# and built for the host ISA as numba compiles for it (4096 x 14336 at 50%,
+# one core: numba 11.4 ms, port 11.2 ms — oracle/Makefile)
+PORT_NOTE = "C port bit-identical to the reference numba kernel, host-ISA build as numba's"
 GEMV_SHAPES = {"q": (4096, 4096), "k": (1024, 4096), "v": (1024, 4096), "o": (4096, 4096),
                "gate": (14336, 4096), "up": (14336, 4096), "down": (4096, 14336)}
 
@@ -73,6 +80,8 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true", help="skip the per-level / per-shape sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--calib-tokens", type=int, default=128, help="dense decode steps whose taps calibrate the thresholds")
+    ap.add_argument("--contexts", default="512,2048", help="extra decode positions timed in the sweep")
     ap.add_argument("--engine", choices=["step", "launch"], default="step")
     ap.add_argument("--tp", action="store_true",
                     help="config 4: tensor-parallel decode over the N ranks (persistent step kernel per rank, "
@@ -243,7 +252,7 @@ def run_reference(args):
     tok_s = 1.0 / statistics.median(samples)
     sample = (f"per step: Llama-3-8B layer-0 q/k/v/o/gate/up/down at s={args.sparsity} (fp32 input-major, "
               f"t=gaussian_threshold) + 1/16 LM-head slice dense; token time = 32 layers + 16 slices; "
-              f"attention excluded (<0.1% at this context)")
+              f"attention excluded (<0.1% at this context); {PORT_NOTE} ({OC.isa_level()} build)")
     line = {"impl": "reference", "metric": METRIC, "value": round(tok_s, 4), "unit": UNIT,
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 / tok_s, 3), "higher_is_better": True, "scaling": "weak",
@@ -294,6 +303,28 @@ def decode_tok_s(D, W, thr, steps, warmup, ws, engine="step", gbs_out=None):
     del dec
     torch.cuda.empty_cache()
     return steps * 1e3 / ms, ms / steps, n
+
+
+def context_tok_s(D, W, thr, ctx: int, steps: int, ws: int) -> float:
+    """Decode tok/s of the step engine at positions [ctx, ctx + steps): the
+    KV cache holds ctx earlier positions (the long-context kernel variant from
+    2048 on, StepDecoder(long_context=4, long_from=2048))."""
+    import dataclasses
+    import torch
+    from paper_2408_14690_b200 import engine as E
+    spec = dataclasses.replace(W.spec, max_seq=max(W.spec.max_seq, ctx + steps + 8))
+    Wc = dataclasses.replace(W, spec=spec)
+    dec = E.StepDecoder(Wc, thr, long_context=4, long_from=2048)
+    dec.reset()
+    dec.capture(from_token=True)
+    dec.reset(start_pos=ctx)
+    for _ in range(3):
+        dec.replay()
+    torch.cuda.synchronize()
+    ms = timed(dec.replay, steps, ws)
+    del dec
+    torch.cuda.empty_cache()
+    return steps * 1e3 / ms
 
 
 def gate_up_roofline(D, C, W, thr, reps: int = 20):
@@ -411,7 +442,7 @@ def run_ours(args):
     peak, peak_src = peak_hbm()
     spec = D.LLAMA3_8B
     W = D.random_weights(spec, torch.bfloat16, seed=rank)
-    hists = D.calibrate_histograms(W, n_tokens=16, seed=1000 + rank)
+    hists = D.calibrate_histograms(W, n_tokens=args.calib_tokens, seed=1000 + rank)
     levels = sorted({float(v) for v in args.levels.split(",")} | {args.sparsity})
     thr = {s: D.uniform_thresholds(hists, spec.n_layers, s) for s in levels}
     torch.cuda.synchronize()
@@ -439,6 +470,8 @@ def run_ours(args):
         roof = {"kernel": "teal step_kernel (persistent decode step, one launch per token)",
                 "per_launch_us": per_launch_us, "algo_bytes": algo, "gbs": algo / (per_launch_us * 1e-6) / 1e9,
                 "kept_frac": kept_frac, "share": 1.0}
+
+    positions = (pos0, pos0 + args.steps - 1) if args.engine == "step" else None
 
     # e2e: same steps through host buffers (H2D token in, D2H argmax out per step)
     dec.reset()
@@ -470,6 +503,13 @@ def run_ours(args):
             dec_rows[str(s)] = round(tok, 2)
             if "gbs" in gl:
                 frac_rows[str(s)] = round(gl["gbs"] / peak, 3)
+        if args.engine == "step" and args.contexts:
+            sweep_ctx = {}
+            for ctx in (int(c) for c in args.contexts.split(",") if c):
+                sweep_ctx[str(ctx)] = round(context_tok_s(D, W, thr[args.sparsity], ctx, n_sw, ws), 2)
+            dec_rows_ctx = sweep_ctx
+        else:
+            dec_rows_ctx = None
         other = "launch" if args.engine == "step" else "step"
         other_rows = {"dense": round(decode_tok_s(D, W, None, n_sw, 3, ws, other)[0], 2),
                       str(args.sparsity): round(decode_tok_s(D, W, thr[args.sparsity], n_sw, 3, ws, other)[0], 2)}
@@ -479,10 +519,11 @@ def run_ours(args):
                  f"{other}_engine_tok_s": other_rows,
                  "dense_weight_gb_per_token": round(wb / 1e9, 3),
                  "dense_hbm_frac": round(dense_tok * wb / 1e9 / peak, 3),
+                 f"decode_tok_s_at_context_{args.sparsity}": dec_rows_ctx,
                  "hbm_roofline_frac": frac_rows}
         del W
         torch.cuda.empty_cache()
-        sweep["gemv_gbs"] = gemv_sweep([0.0, 0.4, 0.5])
+        sweep["gemv_gbs"] = gemv_sweep([0.0, 0.25, 0.4, 0.5, 0.65])
         # config 5: Mistral-7B gate shape, batched shared-mask GEMV at 50 %
         # (device time of graph-captured launches; scripts/batched_sweep.py)
         sys.path.insert(0, str(ROOT / "scripts"))
@@ -494,10 +535,12 @@ def run_ours(args):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         samples = cpu_layer_sample(1, args.sparsity, reps=args.cpu_reps)
+        from oracle import cpu as OC
         cpu = {"value": round(1.0 / statistics.median(samples), 4), "unit": UNIT, "cores": 1, "kind": "port",
                "sample": (f"oracle C port of reference _skip_gemv (kernel.py:30-44), 1 thread, fp32: Llama-3-8B "
                           f"layer-0 7 projections at s={args.sparsity} + 1/16 LM-head slice, x{args.cpu_reps} reps; "
-                          f"token = 32 layers + 16 slices; host has {os.cpu_count()} cores")}
+                          f"token = 32 layers + 16 slices; host has {os.cpu_count()} cores; {PORT_NOTE} "
+                          f"({OC.isa_level()} build)")}
 
     traffic = None
     tp = ROOT / "profiles" / ("step_traffic.json" if args.engine == "step" else "gate_up_traffic.json")
@@ -515,6 +558,8 @@ def run_ours(args):
             "config": {"workload": "llama3-8b random-init batch-1 decode, TEAL uniform calibrated sparsity",
                        "sparsity": args.sparsity, "batch": 1, "weights": "bf16 tiled input-major",
                        "engine": args.engine, "parallelism": "replicas" if ws > 1 else "single",
+                       "positions": f"{positions[0]}..{positions[1]}" if positions else None,
+                       "calibration": f"{args.calib_tokens} dense decode steps (GPU tap histograms)",
                        "l2": "inputs larger than L2 (15 GB of weights per step)"},
             "roofline": {"bound": "hbm", "kernel": roof["kernel"],
                          "achieved": round(roof["gbs"], 1), "peak": peak, "peak_src": peak_src, "unit": "GB/s",

@@ -238,6 +238,37 @@ int teal_argmax(const float* logits, int64_t n, int* out_token,
                 float* ws, uint32_t* tickets, cudaStream_t stream);
 
 
+/* ---- small-batch decode (config 5: B sequences in lockstep) -------------
+ * The projections run in teal_gemv_batched (one shared mask per projection,
+ * sparsifier.sparsify_batched, sparsifier.py:136-155); these are the steps
+ * around them, one launch for all B rows each. */
+
+/* teal_decode_attention for B sequences: q / ctx [B][H*hd], caches
+ * [B][KVH][max_seq][hd] (sequence b's slice at b*KVH*max_seq*hd), *len
+ * positions each (model.py:135-150); ws / tickets: B times the B = 1 sizes. */
+int teal_batch_attention(const float* q, const void* k_cache, const void* v_cache, int kv_dtype, int B, int H,
+                         int KVH, int hd, int64_t max_seq, const int* len, int max_len, float* ctx, float* ws,
+                         uint32_t* tickets, int nsplit, cudaStream_t stream);
+/* x[b] = float(emb[tokens[b]]), x [B][d]; state (nullable) {pos, len}: this
+ * step writes position len (pos = len, len += 1) */
+int teal_batch_embed(const void* emb, int emb_dtype, const int* tokens, int B, int64_t d, float* x, int* state,
+                     cudaStream_t stream);
+/* x[b] += delta[b] (delta nullable); h[b] = x[b] / sqrt(mean(x[b]^2) + eps) * gain
+ * (model.py:126-128 with the residual adds of model.py:184,198) */
+int teal_batch_rmsnorm(float* x, const float* delta, const float* gain, float eps, int B, int64_t d, float* h,
+                       cudaStream_t stream);
+/* RoPE (rotate-half, cos/sin tables [max_seq][hd/2]; NULL: none) of q [B][H][hd]
+ * and k [B][KVH][hd] in place at position state[0]; k and v [B][KVH][hd]
+ * appended to the caches [B][KVH][max_seq][hd] (kv dtype TEAL_BF16 / F32).
+ * Traps when state[0] is outside [0, max_seq). */
+int teal_batch_rope_cache(float* q, float* k, const float* v, void* k_cache, void* v_cache, int kv_dtype,
+                          const float* rope_cos, const float* rope_sin, const int* state, int B, int H, int KVH,
+                          int hd, int64_t max_seq, cudaStream_t stream);
+/* out = SiLU(gate) * up elementwise over n = B * d_ff values (model.py:190-193) */
+int teal_batch_silu_mul(const float* gate, const float* up, int64_t n, float* out, cudaStream_t stream);
+/* tokens[b] = argmax of logits[b] ([B][n]; lowest index on ties, NaN ignored) */
+int teal_batch_argmax(const float* logits, int B, int64_t n, int* tokens, cudaStream_t stream);
+
 /* ---- persistent decode step (one launch per token) ----------------------
  *
  * Replaces the per-projection launches of a decode step (the seven

@@ -10,22 +10,50 @@ from pathlib import Path
 import numpy as np
 
 HERE = Path(__file__).resolve().parent
-LIB = HERE / "build" / "liboracle_teal.so"
+LIB = HERE / "build" / "liboracle_teal.so"          # x86-64-v2 (any x86-64 host)
+LIB_V3 = HERE / "build" / "liboracle_teal_v3.so"    # AVX2 / FMA hosts
+LIB_V4 = HERE / "build" / "liboracle_teal_v4.so"    # AVX-512 hosts
 _lib = None
 
 
 def build(force: bool = False) -> Path:
-    if force or not LIB.exists() or LIB.stat().st_mtime < (HERE / "teal_oracle.c").stat().st_mtime:
+    libs = (LIB, LIB_V3, LIB_V4)
+    src = (HERE / "teal_oracle.c").stat().st_mtime
+    if force or any(not p.exists() or p.stat().st_mtime < src for p in libs):
         subprocess.run(["make", "-C", str(HERE), "-B" if force else "-s"], check=True,
                        capture_output=True, text=True)
     return LIB
+
+
+def isa_level() -> str:
+    """Widest x86-64 level the host supports (numba compiles the reference
+    for the host CPU the same way)."""
+    try:
+        flags = set()
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("flags"):
+                flags = set(line.split(":", 1)[1].split())
+                break
+    except OSError:
+        return "v2"
+    if {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl", "avx2", "fma", "bmi2"} <= flags:
+        return "v4"
+    if {"avx2", "fma", "bmi2", "movbe"} <= flags:
+        return "v3"
+    return "v2"
+
+
+def lib_path() -> Path:
+    lv = isa_level()
+    p = {"v4": LIB_V4, "v3": LIB_V3}.get(lv, LIB)
+    return p if p.exists() else LIB
 
 
 def lib():
     global _lib
     if _lib is None:
         build()
-        L = ctypes.CDLL(str(LIB))
+        L = ctypes.CDLL(str(lib_path()))
         f32p = ctypes.POINTER(ctypes.c_float)
         ll = ctypes.c_longlong
         L.oracle_skip_gemv.argtypes = [f32p, f32p, ll, ll, ctypes.c_double, f32p]

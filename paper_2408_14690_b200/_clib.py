@@ -77,6 +77,15 @@ _SIGNATURES = [
                                              ctypes.c_int, c_vp]),
     ("teal_load_residual", ctypes.c_int, [c_vp, ctypes.c_int, c_vp, c_i64, c_vp, c_vp, ctypes.c_int, c_vp, c_vp]),
     ("teal_argmax", ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    ("teal_batch_attention", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_int, c_i64, c_vp, ctypes.c_int, c_vp, c_vp, c_vp, ctypes.c_int,
+                                            c_vp]),
+    ("teal_batch_embed", ctypes.c_int, [c_vp, ctypes.c_int, c_vp, ctypes.c_int, c_i64, c_vp, c_vp, c_vp]),
+    ("teal_batch_rmsnorm", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_float, ctypes.c_int, c_i64, c_vp, c_vp]),
+    ("teal_batch_rope_cache", ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_vp,
+                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i64, c_vp]),
+    ("teal_batch_silu_mul", ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
+    ("teal_batch_argmax", ctypes.c_int, [c_vp, ctypes.c_int, c_i64, c_vp, c_vp]),
     ("teal_residual_add", ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, ctypes.c_int, c_vp]),
     ("teal_step_ctas_per_sm", ctypes.c_int, [ctypes.c_int]),
     ("teal_gemv_batched_workspace", ctypes.c_int, [ctypes.POINTER(TealGemvBatchedArgs), ctypes.POINTER(ctypes.c_int),

@@ -20,7 +20,8 @@ __global__ void __launch_bounds__(kThreads) attention_kernel(const float* __rest
                                                              const KT* __restrict__ vc, int H, int KVH, int hd,
                                                              int64_t max_seq, const int* __restrict__ len_ptr,
                                                              int chunk, float* __restrict__ ctx,
-                                                             float* __restrict__ ws, uint32_t* __restrict__ tickets) {
+                                                             float* __restrict__ ws, uint32_t* __restrict__ tickets,
+                                                             int64_t kv_bstride) {
     __shared__ float s_q[ATT_MAX_G * ATT_MAX_HD];
     __shared__ float s_sc[ATT_MAX_G * ATT_MAX_CHUNK];
     __shared__ float s_m[ATT_MAX_G], s_l[ATT_MAX_G];
@@ -28,6 +29,17 @@ __global__ void __launch_bounds__(kThreads) attention_kernel(const float* __rest
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int kvh = blockIdx.x, sp = blockIdx.y, nsplit = gridDim.y;
     const int G = H / KVH;
+    // batch (blockIdx.z): sequence b's q / ctx rows, its cache slice and its
+    // split-combine records and tickets
+    {
+        const int b = blockIdx.z;
+        q += (int64_t)b * H * hd;
+        ctx += (int64_t)b * H * hd;
+        kc += (int64_t)b * kv_bstride;
+        vc += (int64_t)b * kv_bstride;
+        if (ws) ws += (int64_t)b * KVH * nsplit * (G * hd + 2 * G);
+        if (tickets) tickets += (int64_t)b * KVH;
+    }
     const int L = *len_ptr;
     const int p0 = sp * chunk;
     const int p1 = min(L, p0 + chunk);
@@ -211,6 +223,21 @@ __global__ void __launch_bounds__(kThreads) argmax_kernel(const float* __restric
 
 using namespace teal;
 
+static int launch_attention(const float* q, const void* k_cache, const void* v_cache, int kv_dtype, int H, int KVH,
+                            int hd, int64_t max_seq, const int* len, int chunk, int nsplit, int B, int64_t kv_bstride,
+                            float* ctx, float* ws, uint32_t* tickets, cudaStream_t stream, const char* what) {
+    dim3 grid(KVH, nsplit, B);
+    if (kv_dtype == TEAL_F32)
+        attention_kernel<float><<<grid, kThreads, 0, stream>>>(q, (const float*)k_cache, (const float*)v_cache, H, KVH, hd,
+                                                               max_seq, len, chunk, ctx, ws, tickets, kv_bstride);
+    else if (kv_dtype == TEAL_BF16)
+        attention_kernel<uint16_t><<<grid, kThreads, 0, stream>>>(q, (const uint16_t*)k_cache, (const uint16_t*)v_cache, H,
+                                                                  KVH, hd, max_seq, len, chunk, ctx, ws, tickets, kv_bstride);
+    else
+        TEAL_REQUIRE(false, "%s: unsupported kv dtype %d", what, kv_dtype);
+    return check_launch(what);
+}
+
 extern "C" {
 
 int teal_decode_attention(const float* q, const void* k_cache, const void* v_cache, int kv_dtype, int H, int KVH, int hd,
@@ -226,16 +253,26 @@ int teal_decode_attention(const float* q, const void* k_cache, const void* v_cac
     TEAL_REQUIRE(chunk <= ATT_MAX_CHUNK, "teal_decode_attention: %d positions per split exceeds %d; raise nsplit",
                  chunk, ATT_MAX_CHUNK);
     TEAL_REQUIRE(nsplit == 1 || (ws && tickets), "teal_decode_attention: nsplit > 1 needs ws and tickets");
-    dim3 grid(KVH, nsplit);
-    if (kv_dtype == TEAL_F32)
-        attention_kernel<float><<<grid, kThreads, 0, stream>>>(q, (const float*)k_cache, (const float*)v_cache, H, KVH, hd,
-                                                               max_seq, len, chunk, ctx, ws, tickets);
-    else if (kv_dtype == TEAL_BF16)
-        attention_kernel<uint16_t><<<grid, kThreads, 0, stream>>>(q, (const uint16_t*)k_cache, (const uint16_t*)v_cache, H,
-                                                                  KVH, hd, max_seq, len, chunk, ctx, ws, tickets);
-    else
-        TEAL_REQUIRE(false, "teal_decode_attention: unsupported kv dtype %d", kv_dtype);
-    return check_launch("teal_decode_attention");
+    return launch_attention(q, k_cache, v_cache, kv_dtype, H, KVH, hd, max_seq, len, chunk, nsplit, 1, 0, ctx, ws,
+                            tickets, stream, "teal_decode_attention");
+}
+
+int teal_batch_attention(const float* q, const void* k_cache, const void* v_cache, int kv_dtype, int B, int H, int KVH,
+                         int hd, int64_t max_seq, const int* len, int max_len, float* ctx, float* ws,
+                         uint32_t* tickets, int nsplit, cudaStream_t stream) {
+    TEAL_REQUIRE(q && k_cache && v_cache && len && ctx, "teal_batch_attention: null pointer");
+    TEAL_REQUIRE(B >= 1 && B <= 65535, "teal_batch_attention: bad batch %d", B);
+    TEAL_REQUIRE(H >= 1 && KVH >= 1 && H % KVH == 0 && H / KVH <= ATT_MAX_G,
+                 "teal_batch_attention: need KVH | H and H/KVH <= %d (H=%d KVH=%d)", ATT_MAX_G, H, KVH);
+    TEAL_REQUIRE(hd >= 1 && hd <= ATT_MAX_HD, "teal_batch_attention: head_dim must be in [1, %d]", ATT_MAX_HD);
+    TEAL_REQUIRE(max_len >= 1 && max_len <= max_seq, "teal_batch_attention: bad max_len %d", max_len);
+    TEAL_REQUIRE(nsplit >= 1, "teal_batch_attention: nsplit must be >= 1");
+    const int chunk = (max_len + nsplit - 1) / nsplit;
+    TEAL_REQUIRE(chunk <= ATT_MAX_CHUNK, "teal_batch_attention: %d positions per split exceeds %d; raise nsplit",
+                 chunk, ATT_MAX_CHUNK);
+    TEAL_REQUIRE(nsplit == 1 || (ws && tickets), "teal_batch_attention: nsplit > 1 needs ws and tickets");
+    return launch_attention(q, k_cache, v_cache, kv_dtype, H, KVH, hd, max_seq, len, chunk, nsplit, B,
+                            (int64_t)KVH * max_seq * hd, ctx, ws, tickets, stream, "teal_batch_attention");
 }
 
 int teal_load_residual(const void* src, int src_dtype, const int* token, int64_t d, float* x, float* ss_out, int tile,

@@ -272,3 +272,20 @@ class TestFusedSegments:
         _, (g, u), inter = self._run(cuda_device, [2816, 2816], 1024, [0.6, 0.7], dtype, epi="silu")
         want = g / (1 + np.exp(-g)) * u
         assert rel_err(inter.cpu().numpy(), want) <= 1e-5
+
+
+@pytest.mark.parametrize("bpe", [4, 2])
+def test_bench_gemv_checks_against_an_independent_product(bpe):
+    # kernel.bench_gemv (kernel.py:133-209): every rep checked after timing
+    # against cuBLAS fp64 of the fp64-masked input (not this package's
+    # kernels), realized sparsity near the Gaussian quantile, MAC-free
+    # traffic model (kernel.py:68-91)
+    import paper_2408_14690_b200 as T
+    r = T.bench_gemv(1024, 4096, [0.0, 0.25, 0.5, 0.65], reps=10, warmup=3, rng=T.RngStream(5),
+                     bytes_per_element=bpe)
+    assert r.rows == 1024 and r.cols == 4096 and len(r.points) == 4
+    for p in r.points:
+        assert p.checksum_ok
+        assert abs(p.realized_sparsity - p.sparsity) < 0.05
+        assert abs(p.traffic.weight_bytes_sparse - (1 - p.realized_sparsity) * 1024 * 4096 * bpe) <= 1
+        assert p.median_ns > 0 and p.min_ns <= p.median_ns
