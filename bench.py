@@ -35,8 +35,15 @@ Line keys beyond the base contract:
 `--impl reference` times the reference CPU path (the oracle port of
 `_skip_gemv`, all host threads, fp32) on the same workload: each step is one
 layer's 7 projections at 50% plus an LM-head slice, extrapolated to a token.
-Multi-GPU: the 8B decode fits one GPU, so N>1 runs N independent replicas
-(weak scaling, no collective on the data path); `value` = N*K / max-rank time.
+Multi-GPU (N > 1, launched by torchrun): config 4 — ONE Llama-3-70B token
+stream decoded tensor-parallel over the N GPUs (column-parallel q/k/v/gate/up,
+row-parallel o/down, vocabulary-parallel LM head; each rank's persistent step
+kernel split at the row-parallel outputs, an NCCL int64 all-reduce of the
+fixed-point accumulators between the pieces, all in one CUDA graph), strong
+scaling, `value` = tokens/s of the stream, device time max over ranks.
+`--fused` runs the variant with the exchange inside the kernel over CUDA-IPC
+peer memory (one launch per token per GPU); `--replicas` the old N
+independent 8B decodes.
 """
 
 from __future__ import annotations
@@ -85,7 +92,9 @@ def parse():
     ap.add_argument("--engine", choices=["step", "launch"], default="step")
     ap.add_argument("--tp", action="store_true",
                     help="config 4: tensor-parallel decode over the N ranks (persistent step kernel per rank, "
-                         "NCCL int64 all-reduce of the row-parallel accumulators) instead of N replicas")
+                         "NCCL int64 all-reduce of the row-parallel accumulators); the default whenever N > 1")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: N independent 8B decodes (weak scaling) instead of config 4")
     ap.add_argument("--tp-model", choices=["8b", "70b"], default="70b")
     ap.add_argument("--fused", action="store_true",
                     help="with --tp: the exchange inside the kernel (peer memory over CUDA IPC / NVLink), "
@@ -327,6 +336,58 @@ def context_tok_s(D, W, thr, ctx: int, steps: int, ws: int) -> float:
     return steps * 1e3 / ms
 
 
+def batch_decode_sweep(peak: float, batches=(1, 2, 4, 8, 16), quants=(None, "int8", "int4"), level: float = 0.5,
+                       steps: int = 20, ws: int = 1):
+    """Config 5: Mistral-7B random-init lockstep decode of B sequences with
+    shared masks (batch.BatchDecoder) at `level`, thresholds calibrated per
+    batch size on batch-mean histograms; tok/s (B x steps / device time) and
+    the step's algorithmic GB/s over the HBM peak.  B = 1 also runs the
+    persistent per-token engine on the same model."""
+    import torch
+    from paper_2408_14690_b200 import batch as BT
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200 import engine as E
+    W = D.random_weights(D.MISTRAL_7B, torch.bfloat16, seed=7)
+    L = D.MISTRAL_7B.n_layers
+    thr = {}
+    for B in batches:
+        thr[B] = BT.calibrate_batch_thresholds(W, B, level, n_steps=32, seed=100 + B, passes=2)
+    out = {}
+    for q in quants:
+        row = {}
+        for B in batches:
+            dec = BT.BatchDecoder(W, thr[B], B, quant=q, count_kept=True)
+            dec.reset()
+            dec.capture()
+            dec.reset()
+            for _ in range(3):
+                dec.replay()
+            torch.cuda.synchronize()
+            dec.kept.zero_()
+            ms = timed(dec.replay, steps, ws)
+            gbs = dec.algorithmic_bytes(dec.kept, steps=steps) / steps / (ms / steps * 1e-3) / 1e9
+            cols = 1.0 - float(dec.kept.sum()) / (steps * L * sum(m for (_, m) in D.MISTRAL_7B.proj_shapes().values()))
+            row[f"B{B}"] = {"tok_s": round(B * steps * 1e3 / ms, 1), "ms_per_step": round(ms / steps, 3),
+                            "hbm_frac": round(gbs / peak, 3), "column_sparsity": round(cols, 3)}
+            del dec
+            torch.cuda.empty_cache()
+        if 1 in batches:
+            dec = E.StepDecoder(W, thr[1], quant=q)
+            dec.reset()
+            dec.capture()
+            dec.reset()
+            for _ in range(3):
+                dec.replay()
+            ms = timed(dec.replay, steps, ws)
+            row["B1_step_engine_tok_s"] = round(steps * 1e3 / ms, 1)
+            del dec
+            torch.cuda.empty_cache()
+        out[q or "bf16"] = row
+    del W
+    torch.cuda.empty_cache()
+    return out
+
+
 def gate_up_roofline(D, C, W, thr, reps: int = 20):
     """Time the fused gate/up launch of every layer back to back (one CUDA
     graph of n_layers launches, weights 7.3 GB > L2) and report its achieved
@@ -444,7 +505,11 @@ def run_ours(args):
     W = D.random_weights(spec, torch.bfloat16, seed=rank)
     hists = D.calibrate_histograms(W, n_tokens=args.calib_tokens, seed=1000 + rank)
     levels = sorted({float(v) for v in args.levels.split(",")} | {args.sparsity})
-    thr = {s: D.uniform_thresholds(hists, spec.n_layers, s) for s in levels}
+    # two-pass calibration: the realized sparsity matches the level label
+    # (pass 1 = the reference's dense-tap recipe; pass 2 re-records the taps
+    # under pass 1's thresholds), decode.calibrate_thresholds
+    thr = {s: (D.calibrate_thresholds(W, s, n_tokens=args.calib_tokens, seed=1000 + rank, passes=2, engine="step")
+               if s > 0 else D.uniform_thresholds(hists, spec.n_layers, s)) for s in levels}
     torch.cuda.synchronize()
 
     # headline: K timed decode steps at the target sparsity, clocks sampled
@@ -503,6 +568,18 @@ def run_ours(args):
             dec_rows[str(s)] = round(tok, 2)
             if "gbs" in gl:
                 frac_rows[str(s)] = round(gl["gbs"] / peak, 3)
+        if args.engine == "step":
+            # greedy block-wise allocation (Algorithm 1) on the decoder, target = the headline level
+            from paper_2408_14690_b200 import greedy as G
+            gtoks = torch.randint(0, spec.vocab, (32,), generator=torch.Generator().manual_seed(77)).tolist()
+            traces = G.greedy_decoder(W, hists, gtoks, G.StepPolicy(0.05))
+            thr_g = G.decoder_greedy_thresholds(traces, hists, args.sparsity)
+            gl = {}
+            gtok, _, _ = decode_tok_s(D, W, thr_g, n_sw, 3, ws, args.engine, gbs_out=gl)
+            greedy_row = {str(args.sparsity): round(gtok, 2), "hbm_frac": round(gl["gbs"] / peak, 3),
+                          "calibration": "32 tokens, alpha 0.05, per-layer block forward error"}
+        else:
+            greedy_row = None
         if args.engine == "step" and args.contexts:
             sweep_ctx = {}
             for ctx in (int(c) for c in args.contexts.split(",") if c):
@@ -520,10 +597,13 @@ def run_ours(args):
                  "dense_weight_gb_per_token": round(wb / 1e9, 3),
                  "dense_hbm_frac": round(dense_tok * wb / 1e9 / peak, 3),
                  f"decode_tok_s_at_context_{args.sparsity}": dec_rows_ctx,
+                 "greedy_decode_tok_s": greedy_row,
                  "hbm_roofline_frac": frac_rows}
         del W
         torch.cuda.empty_cache()
         sweep["gemv_gbs"] = gemv_sweep([0.0, 0.25, 0.4, 0.5, 0.65])
+        # config 5 as a decode: Mistral-7B, B = 1..16, bf16 / int8 / int4 at 50 %
+        sweep["config5_mistral7b_decode_50"] = batch_decode_sweep(peak, ws=ws)
         # config 5: Mistral-7B gate shape, batched shared-mask GEMV at 50 %
         # (device time of graph-captured launches; scripts/batched_sweep.py)
         sys.path.insert(0, str(ROOT / "scripts"))
@@ -559,7 +639,8 @@ def run_ours(args):
                        "sparsity": args.sparsity, "batch": 1, "weights": "bf16 tiled input-major",
                        "engine": args.engine, "parallelism": "replicas" if ws > 1 else "single",
                        "positions": f"{positions[0]}..{positions[1]}" if positions else None,
-                       "calibration": f"{args.calib_tokens} dense decode steps (GPU tap histograms)",
+                       "calibration": f"{args.calib_tokens} decode steps, 2 passes (dense taps, then taps "
+                                      f"under pass-1 thresholds) so realized sparsity matches the level",
                        "l2": "inputs larger than L2 (15 GB of weights per step)"},
             "roofline": {"bound": "hbm", "kernel": roof["kernel"],
                          "achieved": round(roof["gbs"], 1), "peak": peak, "peak_src": peak_src, "unit": "GB/s",
@@ -589,11 +670,17 @@ def run_tp(args):
     kernel and 2 L NCCL all-reduces of d int64 accumulators (+ one all-gather
     of the LM-head argmax candidates)."""
     import torch
+    os.environ.setdefault("NCCL_DEBUG", "INFO")        # communicator lines (nRanks) on stderr
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     ws, rank, local = dist_setup()
     import paper_2408_14690_b200 as T  # noqa: F401
     from paper_2408_14690_b200 import decode as D
     from paper_2408_14690_b200 import engine as E
     from paper_2408_14690_b200 import tp
+    if ws > 1:
+        import torch.distributed as dist
+        print(f"[bench tp] rank {rank}: backend {dist.get_backend()}, comm_nranks {dist.get_world_size()}, "
+              f"device cuda:{local} ({torch.cuda.get_device_name(local)})", file=sys.stderr, flush=True)
     spec = D.LLAMA3_70B if args.tp_model == "70b" else D.LLAMA3_8B
     ls = tp.shard_spec(spec, ws)
     W = E.random_tiled_model(ls, torch.bfloat16, seed=rank)
@@ -655,6 +742,13 @@ def run_tp(args):
     positions = sum(pos0 + i + 1 for i in range(args.steps))
     algo = dec.dec.algorithmic_bytes(dec.dec.kept, steps=args.steps, positions=positions) / args.steps
     gbs = algo / (ms / args.steps * 1e-3) / 1e9
+    per_rank_gbs = [gbs]
+    if ws > 1:  # every rank's own algorithmic bytes over the common step time
+        import torch.distributed as dist
+        t = torch.tensor([gbs], dtype=torch.float64, device="cuda")
+        allt = [torch.zeros_like(t) for _ in range(ws)]
+        dist.all_gather(allt, t)
+        per_rank_gbs = [float(x.item()) for x in allt]
     # e2e: token H2D in, argmax D2H out every step
     tin = torch.ones(1, dtype=torch.int32).pin_memory()
     tout = torch.zeros(1, dtype=torch.int32).pin_memory()
@@ -679,7 +773,8 @@ def run_tp(args):
                        "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "kernel": "teal step_kernel per rank (algorithmic bytes of rank 0 / step time)",
                          "achieved": round(gbs, 1), "peak": peak, "peak_src": peak_src, "unit": "GB/s",
-                         "frac": round(gbs / peak, 4), "traffic": None},
+                         "frac": round(gbs / peak, 4), "traffic": None,
+                         "per_rank_frac": [round(g / peak, 4) for g in per_rank_gbs]},
             "cpu_baseline": None,
             "e2e": {"value": round(args.steps * 1e3 / ms_e2e, 2), "unit": UNIT, "h2d_bytes_per_step": 4,
                     "d2h_bytes_per_step": 4},
@@ -697,7 +792,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
-    if args.tp:
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.tp or (ws > 1 and not args.replicas):
         return run_tp(args)
     return run_ours(args)
 

@@ -295,7 +295,7 @@ class BatchDecoder:
 
 
 def calibrate_batch_histograms(weights: DecoderWeights, batch: int, n_steps: int = 16, seed: int = 0,
-                               bins: int | None = None, quant: str | None = None):
+                               bins: int | None = None, quant: str | None = None, thresholds=None):
     """Per-batch-size calibration (pkg/tests/test_acceptance.py:
     223-239): run ``n_steps`` dense lockstep decode steps of ``batch`` random
     token streams and bin, per (layer, tap), the batch-mean magnitude vector
@@ -305,7 +305,7 @@ def calibrate_batch_histograms(weights: DecoderWeights, batch: int, n_steps: int
     from .sparsifier import DEFAULT_BIN_COUNT, HI_STD_MULTIPLE, ActivationHistogram
     bins = bins or DEFAULT_BIN_COUNT
     spec = weights.spec
-    dec = BatchDecoder(weights, None, batch, quant=quant, taps=True)
+    dec = BatchDecoder(weights, thresholds, batch, quant=quant, taps=True)
     dec.reset()
     g = torch.Generator(device=dec.device).manual_seed(seed)
     hists = {}
@@ -323,6 +323,20 @@ def calibrate_batch_histograms(weights: DecoderWeights, batch: int, n_steps: int
     del dec
     torch.cuda.empty_cache()
     return hists
+
+
+def calibrate_batch_thresholds(weights: DecoderWeights, batch: int, level: float, n_steps: int = 32,
+                               seed: int = 0, passes: int = 2) -> list[list[float]]:
+    """Batch-size-specific thresholds whose realized column sparsity matches
+    ``level``.  The batch-mean statistic is concentrated (averaging B rows), so
+    its quantiles move a lot when upstream projections are sparsified: pass 1
+    calibrates on the dense decode (the reference's recipe), each further pass
+    on the taps seen while decoding with the previous pass's thresholds."""
+    thr = None
+    for _ in range(max(1, passes)):
+        hists = calibrate_batch_histograms(weights, batch, n_steps=n_steps, seed=seed, thresholds=thr)
+        thr = batch_thresholds(hists, weights.spec.n_layers, level)
+    return thr
 
 
 def batch_thresholds(hists, n_layers: int, level: float) -> list[list[float]]:

@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kThreadsTMA, 2) gemv_tma_kernel(const __grid_c
             const int use = me / NS;
             if (use > 0) mbar_wait(&s_empty[s], (uint32_t)((use - 1) & 1));
             s_meta[s] = make_float2(0.f, __int_as_float(-1));
-            mbar_arrive(&s_full[s]);
+            mbar_arrive_expect_tx(&s_full[s], 0u);  // (the same release-arrive as a data entry, no bytes)
         }
         if (lane == 0) {
             if (kcnt0 && A.seg[0].kept) atomicAdd(A.seg[0].kept, (unsigned long long)kcnt0);

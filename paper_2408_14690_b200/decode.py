@@ -426,7 +426,8 @@ PROJ_TAP = {"q": "pre_attn", "k": "pre_attn", "v": "pre_attn", "o": "attn_out",
 
 
 def calibrate_histograms(weights, n_tokens: int = 16, seed: int = 0,
-                         bins: int | None = None, hi_std_multiple: float | None = None, engine: str = "launch"):
+                         bins: int | None = None, hi_std_multiple: float | None = None, engine: str = "launch",
+                         thresholds=None):
     """GPU-side calibration of the decode engine (model.py:268-294 restated for
     the KV-cache decode): run ``n_tokens`` dense decode steps on random tokens
     with the four taps captured, and bin each (layer, tap) vector on the GPU
@@ -442,9 +443,9 @@ def calibrate_histograms(weights, n_tokens: int = 16, seed: int = 0,
         raise ValueError("token calibration needs an embedding (vocab > 0)")
     if engine == "step":
         from .engine import StepDecoder
-        dec = StepDecoder(weights, None, taps=True)
+        dec = StepDecoder(weights, thresholds, taps=True)
     else:
-        dec = SparseDecoder(weights, None, taps=True)
+        dec = SparseDecoder(weights, thresholds, taps=True)
     dec.reset()
     g = torch.Generator(device=dec.device).manual_seed(seed)
     toks = torch.randint(0, spec.vocab, (n_tokens,), device=dec.device, generator=g, dtype=torch.int32)
@@ -461,6 +462,21 @@ def calibrate_histograms(weights, n_tokens: int = 16, seed: int = 0,
                 hists[key].record(h[l])
     del dec
     return hists
+
+
+def calibrate_thresholds(weights, level: float, n_tokens: int = 128, seed: int = 0, passes: int = 2,
+                         engine: str = "step") -> list[list[float]]:
+    """Uniform-level thresholds whose REALIZED sparsity matches ``level``:
+    pass 1 is the reference's calibration (tap histograms of the dense decode,
+    model.py:268-294); every further pass re-records the taps while decoding
+    with the previous pass's thresholds, so taps downstream of sparsified
+    projections (attention output, SiLU*up) are calibrated on the
+    activations they will actually see.  passes=1 is the reference's recipe."""
+    thr = None
+    for _ in range(max(1, passes)):
+        hists = calibrate_histograms(weights, n_tokens=n_tokens, seed=seed, engine=engine, thresholds=thr)
+        thr = uniform_thresholds(hists, weights.spec.n_layers, level)
+    return thr
 
 
 def uniform_thresholds(hists, n_layers: int, level: float) -> list[list[float]]:

@@ -33,7 +33,8 @@ def step(msg):
     print("ok:", msg, flush=True)
 
 
-QUICK = "--quick" in sys.argv  # (initcheck: the per-launch engine and batched kernels only)
+QUICK = "--quick" in sys.argv  # stop after the per-launch decode engine
+TINY = "--tiny" in sys.argv    # threshold, single GEMVs and the toy step kernel only (initcheck)
 g = np.random.default_rng(0)
 # threshold / batched threshold / histogram
 x = torch.randn(5000, device="cuda")
@@ -55,6 +56,16 @@ for n, m in ((200, 333), (1024, 4096)):
     wd = torch.randn(m, n, device="cuda").to(torch.bfloat16)
     T.sparse_gemv(torch.from_numpy(xv).cuda(), 0.5, T.Matrix.from_device(wd))
 step("single sparse / dense GEMV")
+if TINY:
+    from oracle import actsparse_ref as R  # noqa: E402  (weights of the toy block only)
+    blocks = R.gen_model_weights(5, 1, 256, 4, 768)
+    Wt = D.weights_from_blocks(blocks, 4, max_seq=8)
+    dt = E.StepDecoder(Wt, [[0.3, 0.3, 0.3, 0.01, 0.4, 0.4, 0.02]])
+    dt.reset()
+    dt.step_hidden(np.random.default_rng(0).standard_normal(256).astype(np.float32))
+    step("step kernel, toy block")
+    print("sanitize workload done (tiny)")
+    sys.exit(0)
 # batched shared-mask GEMV (FMA and MMA kernels)
 for kind in ("bf16", "int8", "int4"):
     for B in (1, 4, 16):

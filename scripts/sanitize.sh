@@ -8,6 +8,7 @@ for tool in memcheck racecheck synccheck; do
       python scripts/sanitize.py > gpurun_out/sanitizer_$tool.txt 2>&1
   echo "== $tool rc=$?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|sanitize workload done|Error" gpurun_out/sanitizer_$tool.txt | sort | uniq -c | head -8
 done
-timeout -s KILL 900 compute-sanitizer --tool initcheck --print-limit 50 --kernel-name kns=4teal \
-    python scripts/sanitize.py --quick > gpurun_out/sanitizer_initcheck.txt 2>&1
-echo "== initcheck (quick) rc=$?"; grep -E "ERROR SUMMARY|sanitize workload done|Error" gpurun_out/sanitizer_initcheck.txt | sort | uniq -c | head -8
+# initcheck instruments every kernel (torch's initialising writes must be seen)
+timeout -s KILL 900 compute-sanitizer --tool initcheck --print-limit 50 \
+    python scripts/sanitize.py --tiny > gpurun_out/sanitizer_initcheck.txt 2>&1
+echo "== initcheck (tiny) rc=$?"; grep -E "ERROR SUMMARY|sanitize workload done|Error" gpurun_out/sanitizer_initcheck.txt | sort | uniq -c | head -8

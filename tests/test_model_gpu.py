@@ -277,3 +277,40 @@ def test_sparse_prefill_dense_prefix(toy_model):
     assert not torch.equal(mixed[12:], dense[12:]) and not torch.equal(mixed[12:], sparse[12:])
     with pytest.raises(ValueError, match="dense_prefix"):
         T.model_forward_sparse(toy_model, X, cfgs, dense_prefix=-1)
+
+
+@pytest.mark.gpu
+def test_greedy_on_the_gqa_decoder():
+    # Algorithm 1 (greedy.py:76-127) on the Llama-style decoder the step
+    # engine runs: block inputs from the engine's residual versions, all
+    # candidates of a step in one batched forward (identical errors to one
+    # forward per candidate), trace invariants, and the greedy 50% config
+    # driving the persistent engine
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200 import engine as E
+    from paper_2408_14690_b200 import greedy as G
+    spec = D.DecoderSpec(1024, 8, 2, 2816, 2, vocab=1000, rope_theta=500000.0, norm_eps=1e-5, max_seq=64)
+    W = D.random_weights(spec, torch.bfloat16, seed=41)
+    hists = D.calibrate_histograms(W, n_tokens=16, seed=42, engine="step")
+    toks = np.random.default_rng(43).integers(0, spec.vocab, 24).tolist()
+    X = G.decoder_block_inputs(W, toks)
+    pol = G.StepPolicy(0.1)
+    tb = G.greedy_decoder_layer(W, 0, X[0], hists, pol, batched=True)
+    ts = G.greedy_decoder_layer(W, 0, X[0], hists, pol, batched=False)
+    assert [s.chosen for s in tb.steps] == [s.chosen for s in ts.steps]
+    assert np.allclose([s.error for s in tb.steps], [s.error for s in ts.steps], rtol=1e-6)
+    fp = {n: a * b for n, (a, b) in spec.proj_shapes().items()}
+    G.validate_trace(tb, fp)
+    assert tb.steps[-1].block_sparsity >= 1.0 - 1e-12
+    # k / v jump 0 -> 1 in one step at GQA footprints (delta > 1, clamped)
+    kv_steps = [s for s in tb.steps if s.chosen in ("k", "v")]
+    assert all(s.levels[s.chosen] == 1.0 for s in kv_steps)
+    traces = [tb, G.greedy_decoder_layer(W, 1, X[1], hists, pol)]
+    thr = G.decoder_greedy_thresholds(traces, hists, 0.5)
+    dec = E.StepDecoder(W, thr, count_kept=True)
+    dec.reset()
+    for t in toks[:4]:
+        dec.token.fill_(t)
+        dec.step_token()
+    torch.cuda.synchronize()
+    assert int(dec.kept.sum()) > 0
