@@ -76,10 +76,23 @@ def main() -> None:
     exp["out_sparse"] = A.model_forward_sparse(model, X, [cfg0, cfg1])
     exp["out_dense"] = A.model_forward_dense(model, X)
     exp["trace_P"] = np.array([s.block_sparsity for s in trace.steps])
+    # a one-block model whose shapes the persistent step engine tiles (d and
+    # n_q multiples of 256, head_dim 64 | 128, d_ff multiple of 128), with its
+    # own calibration and configs file, for driving the step engine
+    m2 = A.gen_model(A.RngStream(21), 1, 256, 4, 256)
+    M.save_model(OUT / "model256.teal", m2)
+    cal2 = A.RngStream(22).next_generator().standard_normal((4, 32, 256), dtype=np.float32)
+    taps2 = A.calibrate_model(m2, cal2)[0]
+    c2 = A.uniform_config(taps2, 0.5)
+    G.save_configs(OUT / "configs256.txt", [c2], 0.5)
+    X2 = A.RngStream(23).next_generator().standard_normal((12, 256), dtype=np.float32)
+    exp["X256"] = X2
+    exp["out256_sparse"] = A.model_forward_sparse(m2, X2, [c2])
     np.savez_compressed(OUT / "expect.npz", **exp)
     (OUT / "manifest.json").write_text(json.dumps(
         {"reference": "actsparse " + A.__version__, "histograms": names,
-         "files": ["model.teal", "matrix.teal", "trace.txt", "configs.txt"] + names}, indent=1) + "\n")
+         "files": ["model.teal", "matrix.teal", "trace.txt", "configs.txt", "model256.teal", "configs256.txt"]
+         + names}, indent=1) + "\n")
     print("interop fixtures written to", OUT)
 
 

@@ -40,11 +40,12 @@ def T():
     return T
 
 
-def test_model_file_round_trip(T, tmp_path):
-    m = T.load_model(D / "model.teal")
-    assert (len(m.blocks), m.d_model, m.n_heads, m.d_ff) == (2, 64, 4, 176)
+@pytest.mark.parametrize("name,shape", [("model.teal", (2, 64, 4, 176)), ("model256.teal", (1, 256, 4, 256))])
+def test_model_file_round_trip(T, tmp_path, name, shape):
+    m = T.load_model(D / name)
+    assert (len(m.blocks), m.d_model, m.n_heads, m.d_ff) == shape
     T.save_model(tmp_path / "m", m)
-    assert (tmp_path / "m").read_bytes() == (D / "model.teal").read_bytes()
+    assert (tmp_path / "m").read_bytes() == (D / name).read_bytes()
 
 
 def test_matrix_file_round_trip(T, tmp_path):
@@ -110,12 +111,16 @@ def test_reference_configs_drive_the_decode_engines(T, engine):
     from paper_2408_14690_b200 import decode as Dm
     from paper_2408_14690_b200 import engine as E
     from paper_2408_14690_b200.model import decoder_weights
-    m = T.load_model(D / "model.teal")
-    cfgs, _ = T.load_configs(D / "configs.txt")
+    # the step engine tiles d, n_q in multiples of 256: its run uses the
+    # one-block d = 256 model and its reference-written TEALC1 file
+    sfx = "256" if engine == "step" else ""
+    m = T.load_model(D / f"model{sfx}.teal")
+    cfgs, _ = T.load_configs(D / f"configs{sfx}.txt")
     e = _expect()
+    X, want = e[f"X{sfx}"], e[f"out{sfx}_sparse"]
     thr = [[c.thresholds[n] for n in Dm.PROJ] for c in cfgs]
     W = decoder_weights(m, max_seq=16)
     dec = E.StepDecoder(W, thr) if engine == "step" else Dm.SparseDecoder(W, thr)
     dec.reset()
-    errs = [rel_err(dec.step_hidden(e["X"][t]).cpu().numpy(), e["out_sparse"][t]) for t in range(len(e["X"]))]
+    errs = [rel_err(dec.step_hidden(X[t]).cpu().numpy(), want[t]) for t in range(len(X))]
     assert np.median(errs) < 1e-5 and max(errs) < 1e-4, (np.median(errs), max(errs))
