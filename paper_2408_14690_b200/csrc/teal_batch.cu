@@ -32,26 +32,52 @@ __global__ void __launch_bounds__(kThreads) embed_kernel(const ST* __restrict__ 
 }
 
 // one CTA per row: x (+= delta), sum of squares in a fixed order (per-thread
-// strided partials, then block_sum), h = x / sqrt(mean + eps) * gain
+// partials over its float4 slots, then block_sum), h = x / sqrt(mean + eps) * g.
+// Every load of the row is issued before any is consumed (d <= 8192: at most
+// 8 float4 per thread), so the row costs one memory round trip, not d/256.
+constexpr int RMS_V4 = 8;
 __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ delta,
                                                            const float* __restrict__ gain, float eps, int64_t d,
                                                            float* __restrict__ h) {
     __shared__ float s_scr[kWarps + 1];
-    const int b = blockIdx.x;
-    float* xr = x + (int64_t)b * d;
-    const float* dr = delta ? delta + (int64_t)b * d : nullptr;
+    const int b = blockIdx.x, tid = threadIdx.x;
+    float4* xr = reinterpret_cast<float4*>(x + (int64_t)b * d);
+    const float4* dr = delta ? reinterpret_cast<const float4*>(delta + (int64_t)b * d) : nullptr;
+    const float4* gr = reinterpret_cast<const float4*>(gain);
+    float4* hr = reinterpret_cast<float4*>(h + (int64_t)b * d);
+    const int n4 = (int)(d >> 2);
+    float4 v[RMS_V4], dv[RMS_V4], gv[RMS_V4];
+#pragma unroll
+    for (int q = 0; q < RMS_V4; ++q) {  // straight-line: slots past n4 read slot 0 (unused)
+        const int i = tid + q * kThreads;
+        const int ic = i < n4 ? i : 0;
+        v[q] = xr[ic];
+        dv[q] = dr ? dr[ic] : make_float4(0.f, 0.f, 0.f, 0.f);
+        gv[q] = gr[ic];
+    }
     float sq = 0.f;
-    for (int64_t c = threadIdx.x; c < d; c += kThreads) {
-        float v = xr[c];
-        if (dr) {
-            v += dr[c];
-            xr[c] = v;
+#pragma unroll
+    for (int q = 0; q < RMS_V4; ++q) {
+        const int i = tid + q * kThreads;
+        if (i < n4) {
+            if (dr) {
+                v[q].x += dv[q].x; v[q].y += dv[q].y; v[q].z += dv[q].z; v[q].w += dv[q].w;
+                xr[i] = v[q];
+            }
+            sq = fmaf(v[q].x, v[q].x, sq);
+            sq = fmaf(v[q].y, v[q].y, sq);
+            sq = fmaf(v[q].z, v[q].z, sq);
+            sq = fmaf(v[q].w, v[q].w, sq);
         }
-        sq = fmaf(v, v, sq);
     }
     const float den = sqrtf(block_sum(sq, s_scr) / (float)d + eps);
-    float* hr = h + (int64_t)b * d;
-    for (int64_t c = threadIdx.x; c < d; c += kThreads) hr[c] = (xr[c] / den) * gain[c];
+#pragma unroll
+    for (int q = 0; q < RMS_V4; ++q) {
+        const int i = tid + q * kThreads;
+        if (i < n4)
+            hr[i] = make_float4((v[q].x / den) * gv[q].x, (v[q].y / den) * gv[q].y, (v[q].z / den) * gv[q].z,
+                                (v[q].w / den) * gv[q].w);
+    }
 }
 
 // grid (heads q + kv, B); thread = dimension pair (d, d + hd/2)
@@ -153,7 +179,11 @@ int teal_batch_embed(const void* emb, int emb_dtype, const int* tokens, int B, i
 
 int teal_batch_rmsnorm(float* x, const float* delta, const float* gain, float eps, int B, int64_t d, float* h,
                        cudaStream_t stream) {
-    TEAL_REQUIRE(x && gain && h && B >= 1 && d >= 1, "teal_batch_rmsnorm: bad arguments");
+    TEAL_REQUIRE(x && gain && h && B >= 1 && d >= 4 && d % 4 == 0 && d <= 4LL * RMS_V4 * kThreads,
+                 "teal_batch_rmsnorm: need 4 | d <= %d", 4 * RMS_V4 * kThreads);
+    TEAL_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(h) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(gain) & 15) == 0 && (reinterpret_cast<uintptr_t>(delta) & 15) == 0,
+                 "teal_batch_rmsnorm: 16-byte aligned rows");
     rmsnorm_kernel<<<B, kThreads, 0, stream>>>(x, delta, gain, eps, d, h);
     return check_launch("teal_batch_rmsnorm");
 }

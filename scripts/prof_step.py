@@ -19,9 +19,8 @@ ap.add_argument("--vocab", type=int, default=128256)
 a = ap.parse_args()
 spec = D.DecoderSpec(4096, 32, 8, 14336, a.layers, vocab=a.vocab, rope_theta=500000.0, norm_eps=1e-5, max_seq=2048)
 W = D.random_weights(spec, torch.bfloat16, seed=0)
-if a.s > 0:
-    hists = D.calibrate_histograms(W, n_tokens=4)
-    thr = D.uniform_thresholds(hists, spec.n_layers, a.s)
+if a.s > 0:  # the bench's calibration recipe (two passes; launch engine, so no step_kernel launches here)
+    thr = D.calibrate_thresholds(W, a.s, n_tokens=32, passes=2, engine="launch")
 else:
     thr = None
 dec = E.StepDecoder(W, thr)

@@ -165,8 +165,8 @@ def test_identical_streams_decode_like_one_stream():
         one.step()
         four.step()
         torch.cuda.synchronize()
-        for b in range(4):
-            assert rel_err(four.x[b].cpu().numpy(), one.x[0].cpu().numpy()) < 1e-6
+        for b in range(4):  # (B = 1 runs the FMA kernel, B = 4 the mma.sync one: fp32 rounding differs)
+            assert rel_err(four.x[b].cpu().numpy(), one.x[0].cpu().numpy()) < 1e-5
             assert int(four.tokens[b]) == int(one.tokens[0])
 
 
@@ -235,8 +235,11 @@ def _teacher_forced(dec, thr, pos):
         x1, x2 = x[..., : hd // 2], x[..., hd // 2:]
         return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1)
 
-    def spz(a, t):
-        m = a.abs().mean(dim=0) <= float(np.float32(t))
+    def spz_p(a, proj, l):
+        # the shared mask the kernel applied — checked bit-exact against the
+        # oracle's sparsify_batched by _check_masks (a torch mean here could
+        # round a tie the other way)
+        m = dec.masks[proj][l].bool()
         return torch.where(m[None, :], torch.zeros_like(a), a)
 
     worst = {}
@@ -249,9 +252,9 @@ def _teacher_forced(dec, thr, pos):
         pw = dec.pw[l]
         W = {p: pw[p].dequantize() for p in PROJ}
         h = dec.taps["pre_attn"][l]
-        rec("q", dec.tap_q[l], rope((spz(h, t[0]) @ W["q"]).view(B, H, hd)).view(B, nq))
-        k = rope((spz(h, t[1]) @ W["k"]).view(B, KVH, hd))
-        v = (spz(h, t[2]) @ W["v"]).view(B, KVH, hd)
+        rec("q", dec.tap_q[l], rope((spz_p(h, "q", l) @ W["q"]).view(B, H, hd)).view(B, nq))
+        k = rope((spz_p(h, "k", l) @ W["k"]).view(B, KVH, hd))
+        v = (spz_p(h, "v", l) @ W["v"]).view(B, KVH, hd)
         rec("k_row", dec.kcache[l][:, :, pos].float(), k.to(dec.kv_dtype).float())
         rec("v_row", dec.vcache[l][:, :, pos].float(), v.to(dec.kv_dtype).float())
         q = dec.tap_q[l].view(B, H, hd)
@@ -259,11 +262,11 @@ def _teacher_forced(dec, thr, pos):
         ctx = torch.stack([torch.cat([torch.softmax((Ks[b, hh // G] @ q[b, hh]) / math.sqrt(hd), 0) @ Vs[b, hh // G]
                                       for hh in range(H)]) for b in range(B)])
         rec("ctx", dec.taps["attn_out"][l], ctx)
-        rec("o", dec.tap_o[l], spz(dec.taps["attn_out"][l], t[3]) @ W["o"])
+        rec("o", dec.tap_o[l], spz_p(dec.taps["attn_out"][l], "o", l) @ W["o"])
         hm = dec.taps["pre_mlp"][l]
-        gate, up = spz(hm, t[4]) @ W["gate"], spz(hm, t[5]) @ W["up"]
+        gate, up = spz_p(hm, "gate", l) @ W["gate"], spz_p(hm, "up", l) @ W["up"]
         rec("inter", dec.taps["mlp_inter"][l], gate / (1 + torch.exp(-gate)) * up)
-        rec("down", dec.tap_down[l], spz(dec.taps["mlp_inter"][l], t[6]) @ W["down"])
+        rec("down", dec.tap_down[l], spz_p(dec.taps["mlp_inter"][l], "down", l) @ W["down"])
     lg = dec.tap_final @ dec.lm.dequantize()
     rec("logits", dec.logits, lg)
     assert dec.tokens.tolist() == torch.argmax(dec.logits, dim=1).tolist()
