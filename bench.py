@@ -388,6 +388,93 @@ def batch_decode_sweep(peak: float, batches=(1, 2, 4, 8, 16), quants=(None, "int
     return out
 
 
+def cats_vs_teal(peak: float, level: float = 0.5, reps: int = 20):
+    """The paper's input- vs output-sparsity comparison on the GPU, one token
+    through a Llama-3-8B MLP (d 4096, f 14336) at `level`: TEAL (input
+    sparsity: gate, up and down sparse GEMVs on Gaussian-quantile thresholds)
+    against CATS (dense gate GEMV + SiLU, output-sparse up on the SiLU(gate)
+    mask via teal_output_sparse_gemv, down skipping the zero intermediate
+    channels).  Device time of graph-captured launches over two rotating
+    weight copies (> L2); CATS up-kernel GB/s on the rows it read."""
+    import torch
+    from paper_2408_14690_b200.model import cats_gemv
+    from paper_2408_14690_b200.tensor import Matrix, _gemv
+    from paper_2408_14690_b200.theory import gaussian_threshold
+    from paper_2408_14690_b200 import _runtime as RT
+    dev = torch.device("cuda")
+    d, f = 4096, 14336
+    g = torch.Generator(device=dev).manual_seed(3)
+    sets = []
+    for _ in range(2):
+        wg = (torch.randn(d, f, device=dev, generator=g) / d ** 0.5).to(torch.bfloat16)
+        wu_im = (torch.randn(d, f, device=dev, generator=g) / d ** 0.5).to(torch.bfloat16)
+        wd = (torch.randn(f, d, device=dev, generator=g) / f ** 0.5).to(torch.bfloat16)
+        sets.append((Matrix.from_device(wg), Matrix.from_device(wu_im), wu_im.t().contiguous(), Matrix.from_device(wd)))
+    h = torch.randn(d, device=dev, generator=g)
+    t_in = RT.f32_round_down(gaussian_threshold(level))
+    gl0 = h @ sets[0][0].in_major(dev).float()
+    gate0 = gl0 / (1 + torch.exp(-gl0))
+    t_cats = float(torch.quantile(gate0.abs(), level))
+    inter_t = torch.zeros(f, device=dev)
+
+    def teal(k):
+        G_, U_, _, Dn = sets[k % 2]
+        gt = _gemv(G_, h, t_in)
+        up = _gemv(U_, h, t_in)
+        inter_t.copy_(gt / (1 + torch.exp(-gt)) * up)
+        return _gemv(Dn, inter_t, t_in)
+
+    kept = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def cats(k, kc=None):
+        G_, _, Ur, Dn = sets[k % 2]
+        gl = _gemv(G_, h, float("-inf"))
+        gate = gl / (1 + torch.exp(-gl))
+        inter = cats_gemv(Ur, h, gate, t_cats, kept=kc)
+        return _gemv(Dn, inter, 0.0)
+
+    def time_graph(fn):
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            for k in range(3):
+                fn(k)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=st):
+                for k in range(reps):
+                    fn(k)
+        torch.cuda.current_stream().wait_stream(st)
+        gr.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        gr.replay()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) * 1e3 / reps
+
+    us_teal = time_graph(teal)
+    us_cats = time_graph(cats)
+    cats(0, kept)
+    torch.cuda.synchronize()
+    k_up = int(kept.item())
+    # the up kernel alone
+    G_, _, Ur, _ = sets[0]
+    gate_v = gate0.contiguous()
+
+    def up_only(k):
+        return cats_gemv(sets[k % 2][2], h, gate_v, t_cats)
+
+    us_up = time_graph(up_only)
+    del sets
+    torch.cuda.empty_cache()
+    up_bytes = k_up * d * 2 + d * 4 + f * 4 * 2
+    return {"level": level, "teal_mlp_us": round(us_teal, 2), "cats_mlp_us": round(us_cats, 2),
+            "cats_up_kernel_us": round(us_up, 2), "cats_up_kept_rows": k_up,
+            "cats_up_gbs": round(up_bytes / (us_up * 1e-6) / 1e9, 1),
+            "cats_up_hbm_frac": round(up_bytes / (us_up * 1e-6) / 1e9 / peak, 3)}
+
+
 def gate_up_roofline(D, C, W, thr, reps: int = 20):
     """Time the fused gate/up launch of every layer back to back (one CUDA
     graph of n_layers launches, weights 7.3 GB > L2) and report its achieved
@@ -602,6 +689,8 @@ def run_ours(args):
         del W
         torch.cuda.empty_cache()
         sweep["gemv_gbs"] = gemv_sweep([0.0, 0.25, 0.4, 0.5, 0.65])
+        # the paper's input- vs output-sparsity comparison (TEAL vs CATS MLP)
+        sweep["teal_vs_cats_mlp_50"] = cats_vs_teal(peak)
         # config 5 as a decode: Mistral-7B, B = 1..16, bf16 / int8 / int4 at 50 %
         sweep["config5_mistral7b_decode_50"] = batch_decode_sweep(peak, ws=ws)
         # config 5: Mistral-7B gate shape, batched shared-mask GEMV at 50 %

@@ -238,6 +238,17 @@ int teal_argmax(const float* logits, int64_t n, int* out_token,
                 float* ws, uint32_t* tickets, cudaStream_t stream);
 
 
+/* ---- CATS output-sparse GEMV (the paper's output-sparsity baseline) -----
+ * out[j] = keep_j ? gate[j] * (x . W[j, :]) : 0, keep_j = !(|gate_j| <= t32),
+ * W row-major [n][ldw] (output-major: row j = output j's m input weights,
+ * bf16 / fp32), x [m] fp32, gate [n] fp32 (SiLU already applied).  Replaces
+ * the up-projection of mlp_forward_output_sparse (model.py:331-341) at
+ * decode time: only the rows of kept outputs are read.  keep_bits (nullable)
+ * [ceil(n/32)], kept (nullable) += kept outputs.  m <= 16384. */
+int teal_output_sparse_gemv(const void* w, int w_dtype, int64_t n, int64_t m, int64_t ldw, const float* x,
+                            const float* gate, float t32, float* out, uint32_t* keep_bits,
+                            unsigned long long* kept, cudaStream_t stream);
+
 /* ---- small-batch decode (config 5: B sequences in lockstep) -------------
  * The projections run in teal_gemv_batched (one shared mask per projection,
  * sparsifier.sparsify_batched, sparsifier.py:136-155); these are the steps

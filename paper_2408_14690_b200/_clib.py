@@ -77,6 +77,8 @@ _SIGNATURES = [
                                              ctypes.c_int, c_vp]),
     ("teal_load_residual", ctypes.c_int, [c_vp, ctypes.c_int, c_vp, c_i64, c_vp, c_vp, ctypes.c_int, c_vp, c_vp]),
     ("teal_argmax", ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    ("teal_output_sparse_gemv", ctypes.c_int, [c_vp, ctypes.c_int, c_i64, c_i64, c_i64, c_vp, c_vp, ctypes.c_float,
+                                               c_vp, c_vp, c_vp, c_vp]),
     ("teal_batch_attention", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_int, c_i64, c_vp, ctypes.c_int, c_vp, c_vp, c_vp, ctypes.c_int,
                                             c_vp]),

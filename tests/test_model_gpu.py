@@ -317,3 +317,50 @@ def test_greedy_on_the_gqa_decoder():
         dec.step_token()
     torch.cuda.synchronize()
     assert int(dec.kept.sum()) > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("level", [0.0, 0.5, 0.9])
+def test_cats_output_sparse_gemv(dtype, level):
+    # CATS (model.py:331-341): out[j] = gate[j] * (x . W_up[j]) where |gate_j|
+    # > fl32(t); only kept rows are read.  Mask bit-exact vs the oracle's
+    # keep_mask of the gate, values vs torch (fp32 rows: 1e-5; bf16: same
+    # bf16 weights on both sides)
+    import paper_2408_14690_b200 as T
+    from paper_2408_14690_b200.model import cats_gemv
+    g = torch.Generator(device="cuda").manual_seed(5)
+    n, m = 14336, 4096
+    w = torch.randn(n, m, device="cuda", generator=g) / m ** 0.5
+    if dtype == "bf16":
+        w = w.to(torch.bfloat16)
+    x = torch.randn(m, device="cuda", generator=g)
+    gl = torch.randn(n, device="cuda", generator=g)
+    gate = gl / (1 + torch.exp(-gl))
+    t = float(torch.quantile(gate.abs(), level)) if level > 0 else 0.0
+    bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    kept = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out = cats_gemv(w, x, gate, t, kept=kept, keep_bits=bits)
+    keep = R.keep_mask(gate.cpu().numpy(), t)
+    assert np.array_equal(bits.cpu().numpy().view(np.uint32), R.pack_bits(keep))
+    assert int(kept.item()) == int(keep.sum())
+    want = torch.where(torch.from_numpy(keep).cuda(), gate * (w.float() @ x), torch.zeros_like(gate))
+    assert rel_err(out.cpu().numpy(), want.cpu().numpy()) < 1e-5
+
+
+@pytest.mark.gpu
+def test_cats_mlp_decode_matches_reference_semantics():
+    from paper_2408_14690_b200.model import cats_mlp_decode
+    g = torch.Generator(device="cuda").manual_seed(6)
+    d, f = 1024, 2816
+    wg = torch.randn(d, f, device="cuda", generator=g) / d ** 0.5
+    wu = torch.randn(f, d, device="cuda", generator=g) / d ** 0.5   # row-major W_up
+    wd = torch.randn(f, d, device="cuda", generator=g) / f ** 0.5   # input-major W_down
+    h = torch.randn(d, device="cuda", generator=g)
+    gate = (h @ wg) / (1 + torch.exp(-(h @ wg)))
+    t = float(torch.quantile(gate.abs(), 0.5))
+    out = cats_mlp_decode(wg, wu, wd, h, t)
+    assert not torch.backends.cuda.matmul.allow_tf32  # true fp32 reference GEMVs
+    masked = torch.where(gate.abs() <= float(np.float32(t)), torch.zeros_like(gate), gate)
+    want = (masked * (wu @ h)) @ wd
+    assert rel_err(out.cpu().numpy(), want.cpu().numpy()) < 1e-4
