@@ -249,6 +249,44 @@ int teal_output_sparse_gemv(const void* w, int w_dtype, int64_t n, int64_t m, in
                             const float* gate, float t32, float* out, uint32_t* keep_bits,
                             unsigned long long* kept, cudaStream_t stream);
 
+/* ---- sparse prefill (the prompt pass before decode) ----------------------
+ * TEAL's prefill recipe (not in the reference,
+ * SPEC.md:8): prompt positions t < sparse_from stay dense (attention sinks),
+ * later ones are thresholded with decode's test, then multiplied — per row,
+ * the reference's sparsify + matmul_dense (sparsifier.py:120-134,
+ * tensor.py:130-140).  Two launches:
+ *
+ * teal_prefill_gate: G = mask(X) of X fp32 [T][ldx] (keep = t < sparse_from
+ * || !(|x| <= t32)), written as bf16 x_hi = rn(G) and (x_lo non-NULL)
+ * x_lo = rn(G - x_hi), both [T][ldo]; m, ldx, ldo multiples of 4.  kept
+ * (nullable) += kept values among the thresholded rows.
+ *
+ * teal_prefill_gemm: y[t][:] (+)= (x_hi + x_lo)[t][:] @ W on the tcgen05
+ * tensor cores (TMA-staged, fp32 TMEM accumulator), W bf16 input-major
+ * [m][ldw] (the decode engines' layout); x_lo NULL: one bf16 term.
+ * m multiple of 64, n multiple of 128, 16-byte aligned operands.  A
+ * persistent launch (one CTA per SM, double-buffered TMEM accumulators);
+ * grids smaller than the SM count split K, the last-arriving split summing
+ * the partials in ascending split order (deterministic). */
+typedef struct teal_prefill_args {
+    const void* w;      /* bf16 [m][ldw] */
+    int64_t m, n, ldw;
+    const void* x_hi;   /* bf16 [T][ldx] */
+    const void* x_lo;   /* bf16 [T][ldx] or NULL */
+    int64_t T, ldx;
+    float* y;           /* fp32 [T][ldy] */
+    int64_t ldy;
+    int accumulate;     /* 0: y = G @ W; 1: y += G @ W (residual add) */
+    int splits;         /* K splits: 0 = auto (fill the SMs), 1 = none */
+    float* ws;          /* split-K partials [splits][T][n] (teal_prefill_workspace) or NULL: no split */
+    uint32_t* tickets;  /* [output tiles], zeroed, self-resetting */
+} teal_prefill_args;
+
+int teal_prefill_gate(const float* x, int64_t T, int64_t m, int64_t ldx, float t32, int64_t sparse_from,
+                      void* x_hi, void* x_lo, int64_t ldo, unsigned long long* kept, cudaStream_t stream);
+int teal_prefill_workspace(const teal_prefill_args* a, int* splits, int64_t* ws_floats, int64_t* tickets);
+int teal_prefill_gemm(const teal_prefill_args* a, cudaStream_t stream);
+
 /* ---- small-batch decode (config 5: B sequences in lockstep) -------------
  * The projections run in teal_gemv_batched (one shared mask per projection,
  * sparsifier.sparsify_batched, sparsifier.py:136-155); these are the steps

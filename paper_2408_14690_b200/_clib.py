@@ -52,6 +52,12 @@ class TealGemvBatchedArgs(ctypes.Structure):
                 ("ctas", ctypes.c_int), ("pad_", ctypes.c_int)]
 
 
+class TealPrefillArgs(ctypes.Structure):
+    _fields_ = [("w", c_vp), ("m", c_i64), ("n", c_i64), ("ldw", c_i64), ("x_hi", c_vp), ("x_lo", c_vp),
+                ("T", c_i64), ("ldx", c_i64), ("y", c_vp), ("ldy", c_i64), ("accumulate", ctypes.c_int),
+                ("splits", ctypes.c_int), ("ws", c_vp), ("tickets", c_vp)]
+
+
 # (name, restype, argtypes) for every exported symbol of include/teal_b200.h
 _SIGNATURES = [
     ("teal_last_error", ctypes.c_char_p, []),
@@ -79,6 +85,11 @@ _SIGNATURES = [
     ("teal_argmax", ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     ("teal_output_sparse_gemv", ctypes.c_int, [c_vp, ctypes.c_int, c_i64, c_i64, c_i64, c_vp, c_vp, ctypes.c_float,
                                                c_vp, c_vp, c_vp, c_vp]),
+    ("teal_prefill_gate", ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, ctypes.c_float, c_i64, c_vp, c_vp, c_i64,
+                                         c_vp, c_vp]),
+    ("teal_prefill_workspace", ctypes.c_int, [ctypes.POINTER(TealPrefillArgs), ctypes.POINTER(ctypes.c_int),
+                                              ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
+    ("teal_prefill_gemm", ctypes.c_int, [ctypes.POINTER(TealPrefillArgs), c_vp]),
     ("teal_batch_attention", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_int, c_i64, c_vp, ctypes.c_int, c_vp, c_vp, c_vp, ctypes.c_int,
                                             c_vp]),

@@ -1,0 +1,136 @@
+"""Sparse prefill: the masking pass and the tcgen05 GEMM.
+
+teal_prefill_gate is bit-exact against torch (mask = the reference's
+sparsify test on rows >= sparse_from, sparsifier.py:120-134; bf16 hi / lo
+split).  teal_prefill_gemm is checked against an fp64 product of the SAME
+bf16 operands (the tensor cores multiply bf16 exactly and accumulate in
+fp32: rel 1e-5 at m = 4096), and the two-term path against the fp32 masked product the
+reference computes (rel 2e-5: hi + lo carries x to 2^-18).
+"""
+
+from __future__ import annotations
+
+import pytest
+import torch
+
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2408_14690_b200 import prefill
+    return prefill
+
+
+def _ref_gate(x, t, sparse_from):
+    t32 = torch.tensor(t, dtype=torch.float32).item()
+    keep = ~(x.abs() <= t32)
+    keep[:sparse_from] = True
+    return torch.where(keep, x, torch.zeros_like(x)), keep
+
+
+def rel_err(a, b):
+    a, b = a.double(), b.double()
+    return float((a - b).norm() / b.norm().clamp_min(1e-300))
+
+
+def _case(T, m, n=128, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn(T, m, device="cuda", generator=g)
+    w = (torch.randn(m, n, device="cuda", generator=g) / m ** 0.5).bfloat16()
+    return x, w
+
+
+@pytest.mark.parametrize("T,m,sparse_from,t", [(1, 64, 0, 0.5), (37, 256, 5, 0.8), (300, 4096, 64, 0.67),
+                                                (5, 128, 9, 0.0), (16, 64, 0, float("inf"))])
+def test_gate_bit_exact(P, T, m, sparse_from, t):
+    x, _ = _case(T, m)
+    x[0, :3] = torch.tensor([float("nan"), 0.0, -0.0])
+    kept = torch.zeros(1, dtype=torch.int64, device="cuda")
+    hi, lo = P.gate(x, t, sparse_from, terms=2, kept=kept)
+    g, keep = _ref_gate(x, t, sparse_from)
+    want_hi = g.bfloat16()
+    want_lo = (g - want_hi.float()).bfloat16()
+    assert torch.equal(hi.view(torch.int16), want_hi.view(torch.int16))
+    assert torch.equal(lo.view(torch.int16), want_lo.view(torch.int16))
+    assert kept.item() == int(keep[sparse_from:].sum())
+    hi1, lo1 = P.gate(x, t, sparse_from, terms=1)
+    assert lo1 is None and torch.equal(hi1.view(torch.int16), want_hi.view(torch.int16))
+
+
+@pytest.mark.parametrize("T,m,n", [(1, 64, 128), (128, 64, 128), (129, 256, 256), (77, 512, 384),
+                                   (300, 4096, 1024), (512, 4096, 4096)])
+def test_gemm_one_term_exact_operands(P, T, m, n):
+    x, w = _case(T, m, n, seed=T + m)
+    hi = x.bfloat16()
+    y = P.gemm(w, hi)
+    want = hi.double() @ w.double()
+    assert rel_err(y, want) < 1e-5  # fp32 accumulation in the tensor core over m terms
+
+
+@pytest.mark.parametrize("T,m,n,sparse_from", [(64, 256, 128, 0), (200, 1024, 512, 32), (384, 4096, 1024, 100)])
+def test_masked_gemm_matches_fp32_reference(P, T, m, n, sparse_from):
+    x, w = _case(T, m, n, seed=7 + T)
+    t = 0.6
+    y = P.masked_gemm(x, w, t, sparse_from=sparse_from)
+    g, _ = _ref_gate(x, t, sparse_from)
+    want = g.double() @ w.double()
+    assert rel_err(y, want) < 2e-5
+    # rows before sparse_from are the dense product
+    dense = x[:sparse_from].double() @ w.double()
+    if sparse_from:
+        assert rel_err(y[:sparse_from], dense) < 2e-5
+
+
+@pytest.mark.parametrize("splits", [1, 2, 3, 0])
+def test_split_k_is_deterministic(P, splits):
+    # K split across CTAs, partials summed by the last arriver in split order:
+    # identical bits on every run, and the same product as one split
+    T, m, n = 70, 1024, 256
+    x, w = _case(T, m, n, seed=11)
+    hi, lo = P.gate(x, 0.5, 3)
+    ys = [P.gemm(w, hi, lo, splits=splits) for _ in range(3)]
+    assert all(torch.equal(ys[0], y) for y in ys[1:])
+    g, _ = _ref_gate(x, 0.5, 3)
+    assert rel_err(ys[0], g.double() @ w.double()) < 2e-5
+    base = torch.randn(T, n, device="cuda")
+    acc = base.clone()
+    P.gemm(w, hi, lo, out=acc, accumulate=True, splits=splits)
+    assert rel_err(acc, base.double() + g.double() @ w.double()) < 2e-5
+
+
+def test_persistent_many_units(P):
+    # more tiles than SMs: every CTA loops over several units (TMEM double buffer, smem ring wrap)
+    T, m, n = 1000, 320, 4096
+    x, w = _case(T, m, n, seed=5)
+    y = P.masked_gemm(x, w, 0.4, sparse_from=10)
+    g, _ = _ref_gate(x, 0.4, 10)
+    assert rel_err(y, g.double() @ w.double()) < 2e-5
+
+
+def test_accumulate_and_ragged_tail(P):
+    T, m, n = 131, 192, 256
+    x, w = _case(T, m, n, seed=3)
+    base = torch.randn(T, n, device="cuda")
+    y = base.clone()
+    P.masked_gemm(x, w, 0.3, sparse_from=7, out=y, accumulate=True)
+    g, _ = _ref_gate(x, 0.3, 7)
+    assert rel_err(y, base.double() + g.double() @ w.double()) < 2e-5
+    # a strided output row (ldy > n) leaves the padding untouched
+    wide = torch.full((T, n + 64), 7.0, device="cuda")
+    P.gemm(w, *P.gate(x, 0.3, 7), out=wide[:, :n])
+    assert torch.all(wide[:, n:] == 7.0)
+    assert rel_err(wide[:, :n], g.double() @ w.double()) < 2e-5
+
+
+def test_rejects_bad_shapes(P):
+    from paper_2408_14690_b200._clib import TealError  # noqa: F401
+    x, w = _case(4, 96, 128)
+    with pytest.raises(Exception, match="multiple of 64"):
+        P.masked_gemm(x, w, 0.5)
+    x, w = _case(4, 64, 96)
+    with pytest.raises(Exception, match="multiple"):
+        P.masked_gemm(x, w, 0.5)
+    with pytest.raises(ValueError, match="sparse_from"):
+        P.gate(x, 0.5, sparse_from=-1)
