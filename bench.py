@@ -686,6 +686,10 @@ def run_ours(args):
                  f"decode_tok_s_at_context_{args.sparsity}": dec_rows_ctx,
                  "greedy_decode_tok_s": greedy_row,
                  "hbm_roofline_frac": frac_rows}
+        # sparse prefill (the paper's second-half recipe) on the tcgen05 masked GEMM: TTFT
+        sys.path.insert(0, str(ROOT / "scripts"))
+        import prefill_ttft
+        sweep["prefill_llama3_8b"] = prefill_ttft.run(W, thr[args.sparsity], lengths=(512, 2048), reps=3)
         del W
         torch.cuda.empty_cache()
         sweep["gemv_gbs"] = gemv_sweep([0.0, 0.25, 0.4, 0.5, 0.65])

@@ -286,6 +286,12 @@ int teal_prefill_gate(const float* x, int64_t T, int64_t m, int64_t ldx, float t
                       void* x_hi, void* x_lo, int64_t ldo, unsigned long long* kept, cudaStream_t stream);
 int teal_prefill_workspace(const teal_prefill_args* a, int* splits, int64_t* ws_floats, int64_t* tickets);
 int teal_prefill_gemm(const teal_prefill_args* a, cudaStream_t stream);
+/* RoPE of the prompt rows (rotate-half, as teal_batch_rope_cache; row t is
+ * position pos0 + t): q [T][ldq] rotated in place, rotated k [T][ldk] and v
+ * [T][ldv] written to the caches [KVH][max_seq][hd] rows pos0 .. pos0+T-1. */
+int teal_prefill_rope_cache(float* q, int64_t ldq, const float* k, int64_t ldk, const float* v, int64_t ldv, int T,
+                            int H, int KVH, int hd, int64_t pos0, const float* rope_cos, const float* rope_sin,
+                            void* k_cache, void* v_cache, int kv_dtype, int64_t max_seq, cudaStream_t stream);
 
 /* ---- small-batch decode (config 5: B sequences in lockstep) -------------
  * The projections run in teal_gemv_batched (one shared mask per projection,

@@ -90,6 +90,9 @@ _SIGNATURES = [
     ("teal_prefill_workspace", ctypes.c_int, [ctypes.POINTER(TealPrefillArgs), ctypes.POINTER(ctypes.c_int),
                                               ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     ("teal_prefill_gemm", ctypes.c_int, [ctypes.POINTER(TealPrefillArgs), c_vp]),
+    ("teal_prefill_rope_cache", ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, ctypes.c_int, ctypes.c_int,
+                                               ctypes.c_int, ctypes.c_int, c_i64, c_vp, c_vp, c_vp, c_vp, ctypes.c_int,
+                                               c_i64, c_vp]),
     ("teal_batch_attention", ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_int, c_i64, c_vp, ctypes.c_int, c_vp, c_vp, c_vp, ctypes.c_int,
                                             c_vp]),

@@ -331,6 +331,48 @@ __global__ void __launch_bounds__(256) prefill_gate_kernel(const float* __restri
     }
 }
 
+// RoPE (rotate-half, as teal_batch_rope_cache) of the prompt's q rows in place
+// and k rows into the cache, v rows copied; prompt row t is position pos0 + t
+template <typename KT>
+__global__ void __launch_bounds__(128) prefill_rope_cache_kernel(float* __restrict__ q, int64_t ldq,
+                                                                 const float* __restrict__ k, int64_t ldk,
+                                                                 const float* __restrict__ v, int64_t ldv, int H,
+                                                                 int KVH, int hd, int64_t pos0,
+                                                                 const float* __restrict__ cosv,
+                                                                 const float* __restrict__ sinv, KT* __restrict__ kc,
+                                                                 KT* __restrict__ vc, int64_t max_seq) {
+    const int head = blockIdx.y, half = hd >> 1;
+    const int64_t t = blockIdx.x, pos = pos0 + t;
+    for (int dd = threadIdx.x; dd < half; dd += blockDim.x) {
+        const float cs = cosv ? cosv[pos * half + dd] : 1.f;
+        const float sn = sinv ? sinv[pos * half + dd] : 0.f;
+        if (head < H) {
+            float* r = q + t * ldq + (int64_t)head * hd;
+            const float x0 = r[dd], x1 = r[dd + half];
+            r[dd] = fmaf(-x1, sn, x0 * cs);
+            r[dd + half] = fmaf(x0, sn, x1 * cs);
+        } else {
+            const int kh = head - H;
+            const float* r = k + t * ldk + (int64_t)kh * hd;
+            const float x0 = r[dd], x1 = r[dd + half];
+            const float k0 = fmaf(-x1, sn, x0 * cs), k1 = fmaf(x0, sn, x1 * cs);
+            const float* vr = v + t * ldv + (int64_t)kh * hd;
+            const int64_t off = ((int64_t)kh * max_seq + pos) * hd;
+            if constexpr (sizeof(KT) == 2) {
+                kc[off + dd] = f32_to_bf16_rn(k0);
+                kc[off + dd + half] = f32_to_bf16_rn(k1);
+                vc[off + dd] = f32_to_bf16_rn(vr[dd]);
+                vc[off + dd + half] = f32_to_bf16_rn(vr[dd + half]);
+            } else {
+                kc[off + dd] = k0;
+                kc[off + dd + half] = k1;
+                vc[off + dd] = vr[dd];
+                vc[off + dd + half] = vr[dd + half];
+            }
+        }
+    }
+}
+
 // ---- host side -------------------------------------------------------------
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -489,6 +531,32 @@ int teal_prefill_gemm(const teal_prefill_args* a, cudaStream_t stream) {
     const bool two = a->x_lo != nullptr;
     if (bn_for(a->T, a->n) == 128) return two ? launch<128, 2, 6>(a, sh, stream) : launch<128, 1, 6>(a, sh, stream);
     return two ? launch<256, 2, 4>(a, sh, stream) : launch<256, 1, 4>(a, sh, stream);
+}
+
+int teal_prefill_rope_cache(float* q, int64_t ldq, const float* k, int64_t ldk, const float* v, int64_t ldv, int T,
+                            int H, int KVH, int hd, int64_t pos0, const float* rope_cos, const float* rope_sin,
+                            void* k_cache, void* v_cache, int kv_dtype, int64_t max_seq, cudaStream_t stream) {
+    TEAL_REQUIRE(q && k && v && k_cache && v_cache, "teal_prefill_rope_cache: null pointer");
+    TEAL_REQUIRE(T >= 0 && H >= 1 && KVH >= 1 && H % KVH == 0 && hd >= 2 && hd % 2 == 0,
+                 "teal_prefill_rope_cache: bad shape T=%d H=%d KVH=%d hd=%d", T, H, KVH, hd);
+    TEAL_REQUIRE(ldq >= (int64_t)H * hd && ldk >= (int64_t)KVH * hd && ldv >= (int64_t)KVH * hd,
+                 "teal_prefill_rope_cache: bad row strides");
+    TEAL_REQUIRE(pos0 >= 0 && pos0 + T <= max_seq,
+                 "teal_prefill_rope_cache: positions [%lld, %lld) exceed the cache (max_seq %lld)", (long long)pos0,
+                 (long long)(pos0 + T), (long long)max_seq);
+    if (T == 0) return TEAL_OK;
+    const dim3 grid((unsigned)T, (unsigned)(H + KVH));
+    const int nt = hd / 2 >= 128 ? 128 : (hd / 2 + 31) / 32 * 32;
+    if (kv_dtype == TEAL_BF16)
+        prefill_rope_cache_kernel<uint16_t><<<grid, nt, 0, stream>>>(q, ldq, k, ldk, v, ldv, H, KVH, hd, pos0, rope_cos,
+                                                                     rope_sin, (uint16_t*)k_cache, (uint16_t*)v_cache,
+                                                                     max_seq);
+    else if (kv_dtype == TEAL_F32)
+        prefill_rope_cache_kernel<float><<<grid, nt, 0, stream>>>(q, ldq, k, ldk, v, ldv, H, KVH, hd, pos0, rope_cos,
+                                                                  rope_sin, (float*)k_cache, (float*)v_cache, max_seq);
+    else
+        TEAL_REQUIRE(false, "teal_prefill_rope_cache: unsupported kv dtype %d", kv_dtype);
+    return check_launch("teal_prefill_rope_cache");
 }
 
 }  // extern "C"

@@ -31,8 +31,8 @@ def gate(x: torch.Tensor, t: float, sparse_from: int = 0, terms: int = 2, kept=N
     kept values among the thresholded rows."""
     if terms not in (1, 2):
         raise ValueError(f"terms must be 1 or 2, got {terms}")
-    if not t >= 0.0:
-        raise ValueError(f"threshold must be non-negative, got {t}")
+    if not (t >= 0.0 or t == float("-inf")):
+        raise ValueError(f"threshold must be non-negative (or -inf: dense), got {t}")
     if sparse_from < 0:
         raise ValueError(f"sparse_from must be >= 0, got {sparse_from}")
     xd = x.float().contiguous()
@@ -95,3 +95,174 @@ def masked_gemm(x: torch.Tensor, w: torch.Tensor, t: float, sparse_from: int = 0
     dense): gate + tensor-core GEMM, two launches."""
     hi, lo = gate(x, t, sparse_from, terms, kept)
     return gemm(w, hi, lo, out, accumulate)
+
+
+# ---- the prompt pass of a decoder ----------------------------------------------
+
+PROJ = ("q", "k", "v", "o", "gate", "up", "down")
+
+
+def _thr(t) -> float:
+    return float("-inf") if t is None or t == float("-inf") else float(t)
+
+
+class PrefillResult:
+    """x: final residual rows [T, d]; logits: [T or 1, vocab] (None without an
+    LM head); next_token: argmax of the last position (None without an LM
+    head); kept: per-layer kept counts [L, 7] over the thresholded rows."""
+
+    def __init__(self, x, logits, next_token, kept):
+        self.x, self.logits, self.next_token, self.kept = x, logits, next_token, kept
+
+
+class SparsePrefill:
+    """TEAL's prompt pass for a ``DecoderWeights`` model (bf16 weights):
+    every projection is ``masked_gemm`` (gate + tcgen05 GEMM) with the
+    decoder's per-layer thresholds (q, k, v, o, gate, up, down) applied to
+    prompt rows >= ``sparse_from`` — by default the second half of the
+    prompt, the paper's recipe for log-likelihood evaluation (PAPER.md:269-270,
+    :444) — and the first rows dense (attention sinks).  RMSNorm, SiLU*up and
+    the LM-head argmax are this package's batch kernels; RoPE + K/V cache
+    writes are ``teal_prefill_rope_cache``; causal attention over the cached
+    K/V is torch's scaled_dot_product_attention (library attention, as
+    cuBLAS is a library GEMM).
+
+    With ``decoder`` (a SparseDecoder / StepDecoder over the same weights),
+    the prompt's K/V land in that decoder's cache and the decoder continues
+    at position T from the prompt's argmax token: prefill -> decode.
+    """
+
+    def __init__(self, weights, thresholds=None, terms: int = 2, kv_dtype=None, attention: str = "fp32"):
+        W = weights
+        if W.dtype != torch.bfloat16:
+            raise ValueError("the prefill GEMM takes bf16 weights")
+        if attention not in ("fp32", "bf16"):
+            raise ValueError(f"attention must be 'fp32' or 'bf16', got {attention!r}")
+        self.w, self.spec, self.terms, self.attention = W, W.spec, terms, attention
+        L = self.spec.n_layers
+        thr = [[None] * 7 for _ in range(L)] if thresholds is None else [list(t) for t in thresholds]
+        if len(thr) != L or any(len(t) != 7 for t in thr):
+            raise ValueError(f"need {L} per-layer threshold lists of 7 (q,k,v,o,gate,up,down)")
+        self.thresholds = [[_thr(x) for x in t] for t in thr]
+        self.kv_dtype = kv_dtype or W.dtype
+        spec = self.spec
+        hd = spec.head_dim
+        if spec.rope_theta is not None:
+            inv = 1.0 / (spec.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.float64) / hd))
+            ang = torch.arange(spec.max_seq, dtype=torch.float64)[:, None] * inv[None, :]
+            dev = W.layers[0].wqkv.device
+            self.rope_cos = torch.cos(ang).float().to(dev).contiguous()
+            self.rope_sin = torch.sin(ang).float().to(dev).contiguous()
+        else:
+            self.rope_cos = self.rope_sin = None
+
+    def _attend(self, q, kc, vc, T):
+        """Causal attention of the prompt rows over the cached (kv-dtype) keys
+        and values: fp32 (fused memory-efficient kernel; the decode engine's
+        arithmetic: fp32 q, fp32 softmax) or bf16 (flash kernel, q rounded)."""
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        spec = self.spec
+        G, hd = spec.n_heads // spec.n_kv_heads, spec.head_dim
+        qh = q.view(T, spec.n_heads, hd).transpose(0, 1).unsqueeze(0)
+        if self.attention == "fp32":
+            kk = kc[:, :T].float().repeat_interleave(G, dim=0).unsqueeze(0)
+            vv = vc[:, :T].float().repeat_interleave(G, dim=0).unsqueeze(0)
+            with sdpa_kernel([SDPBackend.EFFICIENT_ATTENTION, SDPBackend.MATH]):
+                ctx = torch.nn.functional.scaled_dot_product_attention(qh, kk, vv, is_causal=True)
+        else:
+            kk = kc[:, :T].to(torch.bfloat16).repeat_interleave(G, dim=0).unsqueeze(0)
+            vv = vc[:, :T].to(torch.bfloat16).repeat_interleave(G, dim=0).unsqueeze(0)
+            with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION, SDPBackend.MATH]):
+                ctx = torch.nn.functional.scaled_dot_product_attention(qh.to(torch.bfloat16), kk, vv, is_causal=True)
+        return ctx[0].transpose(0, 1).reshape(T, spec.n_q).float().contiguous()
+
+    # one projection: y (+)= g(x) @ w[:, c0:c0+n]
+    def _proj(self, x, w, t, sf, out=None, accumulate=False, kept=None):
+        if t == float("-inf"):
+            hi, lo = gate(x, float("-inf"), 0, self.terms)
+        else:
+            hi, lo = gate(x, t, sf, self.terms, kept)
+        return gemm(w, hi, lo, out=out, accumulate=accumulate)
+
+    def forward(self, tokens=None, hidden=None, sparse_from: int | None = None, decoder=None, logits: str = "last",
+                kv_cache=None) -> PrefillResult:
+        """Run the prompt (``tokens`` [T] int, or ``hidden`` rows [T, d]).
+        ``sparse_from`` default T // 2.  ``logits``: "last", "all" or "none".
+        ``kv_cache``: (k, v) tensors [L, KVH, max_seq, hd] to fill (default:
+        the decoder's, else fresh ones)."""
+        spec, W = self.spec, self.w
+        d, f, nq, nkv, hd = spec.d_model, spec.d_ff, spec.n_q, spec.n_kv, spec.head_dim
+        dev = W.layers[0].wqkv.device
+        L = C.lib()
+        sh = RT.stream_handle()
+        if (tokens is None) == (hidden is None):
+            raise ValueError("pass exactly one of tokens / hidden")
+        if tokens is not None:
+            if W.embedding is None:
+                raise ValueError("this model has no embedding: pass hidden rows")
+            tok = torch.as_tensor(tokens, dtype=torch.int32).reshape(-1).to(dev).contiguous()
+            T = tok.numel()
+            x = torch.empty(T, d, device=dev)
+            C.check(L.teal_batch_embed(W.embedding.data_ptr(), RT.dtype_code(W.embedding.dtype), tok.data_ptr(), T, d,
+                                       x.data_ptr(), None, sh))
+        else:
+            h0 = hidden if isinstance(hidden, torch.Tensor) else torch.from_numpy(
+                __import__("numpy").ascontiguousarray(hidden, dtype="float32"))
+            x = h0.to(dev, torch.float32).reshape(-1, d).clone()
+            T = x.shape[0]
+        if T < 1 or T > spec.max_seq:
+            raise ValueError(f"prompt length {T} outside [1, max_seq={spec.max_seq}]")
+        sf = T // 2 if sparse_from is None else int(sparse_from)
+        if sf < 0:
+            raise ValueError(f"sparse_from must be >= 0, got {sf}")
+        if kv_cache is not None:
+            kc_all, vc_all = kv_cache
+        elif decoder is not None:
+            kc_all, vc_all = decoder.kcache, decoder.vcache
+        else:
+            kc_all = torch.zeros(spec.n_layers, spec.n_kv_heads, spec.max_seq, hd, device=dev, dtype=self.kv_dtype)
+            vc_all = torch.zeros_like(kc_all)
+        kvc = RT.dtype_code(kc_all.dtype)
+        kept = torch.zeros(spec.n_layers, 7, dtype=torch.int64, device=dev)
+        h = torch.empty(T, d, device=dev)
+        q = torch.empty(T, nq, device=dev)
+        k = torch.empty(T, nkv, device=dev)
+        v = torch.empty(T, nkv, device=dev)
+        g = torch.empty(T, f, device=dev)
+        u = torch.empty(T, f, device=dev)
+        inter = torch.empty(T, f, device=dev)
+        for l, lw in enumerate(W.layers):
+            t = self.thresholds[l]
+            C.check(L.teal_batch_rmsnorm(x.data_ptr(), None, lw.rms_attn.data_ptr(), spec.norm_eps, T, d,
+                                         h.data_ptr(), sh))
+            self._proj(h, lw.wqkv[:, :nq], t[0], sf, out=q, kept=kept[l, 0])
+            self._proj(h, lw.wqkv[:, nq:nq + nkv], t[1], sf, out=k, kept=kept[l, 1])
+            self._proj(h, lw.wqkv[:, nq + nkv:], t[2], sf, out=v, kept=kept[l, 2])
+            kc, vc = kc_all[l], vc_all[l]
+            C.check(L.teal_prefill_rope_cache(q.data_ptr(), nq, k.data_ptr(), nkv, v.data_ptr(), nkv, T,
+                                              spec.n_heads, spec.n_kv_heads, hd, 0, RT.ptr(self.rope_cos),
+                                              RT.ptr(self.rope_sin), kc.data_ptr(), vc.data_ptr(), kvc,
+                                              spec.max_seq, sh))
+            ctx = self._attend(q, kc, vc, T)
+            self._proj(ctx, lw.wo, t[3], sf, out=x, accumulate=True, kept=kept[l, 3])
+            C.check(L.teal_batch_rmsnorm(x.data_ptr(), None, lw.rms_mlp.data_ptr(), spec.norm_eps, T, d,
+                                         h.data_ptr(), sh))
+            self._proj(h, lw.wgu[:, :f], t[4], sf, out=g, kept=kept[l, 4])
+            self._proj(h, lw.wgu[:, f:], t[5], sf, out=u, kept=kept[l, 5])
+            C.check(L.teal_batch_silu_mul(g.data_ptr(), u.data_ptr(), T * f, inter.data_ptr(), sh))
+            self._proj(inter, lw.wdown, t[6], sf, out=x, accumulate=True, kept=kept[l, 6])
+        lg = nxt = None
+        if W.lm_head is not None and logits != "none":
+            rows = x if logits == "all" else x[T - 1:]
+            hn = torch.empty_like(rows)
+            C.check(L.teal_batch_rmsnorm(rows.data_ptr(), None, W.final_norm.data_ptr(), spec.norm_eps, rows.shape[0],
+                                         d, hn.data_ptr(), sh))
+            lg = self._proj(hn, W.lm_head, float("-inf"), 0)
+            toks = torch.empty(lg.shape[0], dtype=torch.int32, device=dev)
+            C.check(L.teal_batch_argmax(lg.data_ptr(), lg.shape[0], lg.shape[1], toks.data_ptr(), sh))
+            nxt = toks[-1:]
+        if decoder is not None:
+            decoder.reset(T)
+            if nxt is not None:
+                decoder.token.copy_(nxt)
+        return PrefillResult(x, lg, nxt, kept)

@@ -134,3 +134,93 @@ def test_rejects_bad_shapes(P):
         P.masked_gemm(x, w, 0.5)
     with pytest.raises(ValueError, match="sparse_from"):
         P.gate(x, 0.5, sparse_from=-1)
+
+
+# ---- the decoder prompt pass ----------------------------------------------------
+
+def _llama_toy(seed=0):
+    from paper_2408_14690_b200 import decode as D
+    spec = D.DecoderSpec(512, 8, 2, 1024, 2, vocab=1024, rope_theta=10000.0, norm_eps=1e-5, max_seq=128)
+    return D.random_weights(spec, torch.bfloat16, seed=seed)
+
+
+def _teacher_forced_decode(W, thr, toks, kv_dtype=None):
+    from paper_2408_14690_b200 import decode as D
+    dec = D.SparseDecoder(W, thr, kv_dtype=kv_dtype)
+    dec.reset()
+    for t in toks.tolist():
+        dec.token.fill_(t)
+        dec.step_token()
+    return dec
+
+
+@pytest.mark.parametrize("sparse", [False, True])
+def test_prefill_matches_token_by_token_decode(P, sparse):
+    # the prompt pass (all rows thresholded: sparse_from = 0) fills the same
+    # K/V cache and last-position logits as stepping the decode engine
+    # through the prompt one token at a time with the same thresholds
+    from paper_2408_14690_b200 import decode as D
+    W = _llama_toy()
+    thr = D.calibrate_thresholds(W, 0.5, n_tokens=16, engine="launch") if sparse else None
+    toks = torch.randint(0, 1024, (48,), generator=torch.Generator().manual_seed(1))
+    dec = _teacher_forced_decode(W, thr, toks, kv_dtype=torch.float32)  # fp32 caches: no rounding flips
+    pf = P.SparsePrefill(W, thr)
+    kc = torch.zeros_like(dec.kcache)
+    vc = torch.zeros_like(dec.vcache)
+    r = pf.forward(tokens=toks, sparse_from=0, kv_cache=(kc, vc))
+    T = len(toks)
+    # sparse: rare mask flips where the two RMSNorm implementations round differently
+    tol = 3e-3 if sparse else 2e-5
+    assert rel_err(kc[:, :, :T], dec.kcache[:, :, :T]) < tol
+    assert rel_err(vc[:, :, :T], dec.vcache[:, :, :T]) < tol
+    assert rel_err(r.logits[0], dec.logits) < tol
+    if sparse:  # realized sparsity of the thresholded rows is near the calibrated level
+        frac = 1 - r.kept.sum().item() / (T * 2 * (3 * 512 + 512 + 2 * 512 + 1024))
+        assert 0.35 < frac < 0.65, frac
+
+
+def test_prefill_hands_off_to_the_decoder(P):
+    # prefill(prompt) then decode == decode through prompt + continuation
+    from paper_2408_14690_b200 import decode as D
+    W = _llama_toy(seed=3)
+    toks = torch.randint(0, 1024, (40,), generator=torch.Generator().manual_seed(2))
+    ref = _teacher_forced_decode(W, None, toks)
+    ref_next = ref.token.clone()
+    ref.step_token()  # one generated step from the argmax token
+    dec = D.SparseDecoder(W, None)
+    dec.reset()
+    r = P.SparsePrefill(W, None).forward(tokens=toks, decoder=dec)  # bf16 caches, as the decoder's
+    assert dec._pos == len(toks) and int(dec.state[1]) == len(toks)
+    assert torch.equal(r.next_token, ref_next)
+    dec.step_token()
+    # bf16 caches: values ~1e-6 apart can round one ulp (2^-8) apart
+    assert rel_err(dec.logits, ref.logits) < 1e-3
+
+
+def test_prefill_dense_prefix_matches_reference_forward(P):
+    # the reference-written d=256 block (tests/golden/interop) with its TEALC1
+    # thresholds: prefill with sparse_from = k reproduces model_forward_sparse
+    # (dense_prefix = k) of the same model with bf16-rounded weights
+    import numpy as np
+    import paper_2408_14690_b200 as T
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200.model import MATRIX_NAMES, TransformerBlock, TransformerModel
+    from paper_2408_14690_b200.tensor import Matrix
+    from conftest import GOLDEN
+    m = T.load_model(GOLDEN / "interop" / "model256.teal")
+    cfgs, _ = T.load_configs(GOLDEN / "interop" / "configs256.txt")
+    X = np.load(GOLDEN / "interop" / "expect.npz")["X256"]
+
+    def rnd(a):
+        return torch.from_numpy(np.ascontiguousarray(a, np.float32)).bfloat16().float().numpy()
+
+    blocks = tuple(TransformerBlock(b.d_model, b.n_heads, b.d_ff,
+                                    {n: Matrix.from_2d(rnd(b.w2d(n)), b.weights[n].layout) for n in MATRIX_NAMES},
+                                    b.rms_attn, b.rms_mlp) for b in m.blocks)
+    mr = TransformerModel(m.d_model, m.n_heads, m.d_ff, blocks)
+    W = T.decoder_weights(mr, dtype=torch.bfloat16, max_seq=64)
+    thr = [[c.thresholds[n] for n in D.PROJ] for c in cfgs]
+    for k in (0, 5, len(X)):
+        want = T.model_forward_sparse(mr, X, cfgs, dense_prefix=k) if k else T.model_forward_sparse(mr, X, cfgs)
+        got = P.SparsePrefill(W, thr, kv_dtype=torch.float32).forward(hidden=X, sparse_from=k).x
+        assert rel_err(got, torch.as_tensor(want).to(got.device)) < 1e-5, k
