@@ -734,11 +734,23 @@ static int launch_w(const KP& P, cudaStream_t st) {
 using namespace teal;
 using namespace teal::batched;
 
+namespace teal {
+bool gemv_tc_eligible(const teal_gemv_batched_args* a);  // teal_gemv_tc.cu: bf16, 4 <= B <= 16
+int64_t gemv_tc_workspace_floats(const teal_gemv_batched_args* a, int64_t* tickets);
+int gemv_tc_launch(const teal_gemv_batched_args* a, cudaStream_t stream);
+}  // namespace teal
+
 extern "C" {
 
 int teal_gemv_batched_workspace(const teal_gemv_batched_args* a, int* ctas, int64_t* ws_floats, int64_t* tickets) {
     int st = validate(a);
     if (st) return st;
+    if (gemv_tc_eligible(a)) {  // tcgen05 path: compaction + tensor-core contraction
+        if (ctas) *ctas = 0;
+        const int64_t f = gemv_tc_workspace_floats(a, tickets);
+        if (ws_floats) *ws_floats = f;
+        return TEAL_OK;
+    }
     KP P;
     memset(&P, 0, sizeof(P));
     plan(a, &P);
@@ -752,6 +764,7 @@ int teal_gemv_batched_workspace(const teal_gemv_batched_args* a, int* ctas, int6
 int teal_gemv_batched(const teal_gemv_batched_args* a, cudaStream_t stream) {
     int st = validate(a);
     if (st) return st;
+    if (gemv_tc_eligible(a)) return gemv_tc_launch(a, stream);
     KP P;
     memset(&P, 0, sizeof(P));
     P.a = *a;

@@ -159,3 +159,30 @@ def test_quantisation_roundtrip_error_small():
     for q, tol in ((Q.quantize_int8(w), 0.01), (Q.quantize_int4(w, 128), 0.12)):
         err = (q.dequantize() - w).norm() / w.norm()
         assert float(err) < tol
+
+
+@pytest.mark.parametrize("B", [4, 7, 13, 16])
+def test_tcgen05_path_ragged(B):
+    """The tcgen05 route (bf16, B >= 4, n >= 64 * 128): compaction of a ragged
+    m (a partial 1024-column chunk), padded K blocks, deterministic split K,
+    dense (t None) and all-pruned thresholds; mask bit-exact, product at the
+    fp32 bar (bf16 hi + lo activations: rel 1e-5) against float64, kept count
+    = the oracle's, and identical bits on a repeat."""
+    from paper_2408_14690_b200 import quant as Q
+    m, n = 3000, 8192
+    xs, w = _case(900 + B, B, m, n)
+    qw = Q.as_bf16(torch.from_numpy(w).cuda())
+    wd = qw.dequantize().cpu().numpy().astype(np.float64)
+    for t in (None, 0.0, 0.6745, 1.5, 1e9):
+        kept = torch.zeros(1, dtype=torch.int64, device="cuda")
+        y, mask = Q.sparse_gemv_batched(xs, t, qw, return_mask=True, kept=kept)
+        y2 = Q.sparse_gemv_batched(xs, t, qw)
+        assert np.array_equal(np.asarray(y), np.asarray(y2)), (B, t)
+        xs_s, mref = (xs, np.zeros(m, np.uint8)) if t is None else R.sparsify_batched(xs, t)
+        assert np.array_equal(mask, mref), (B, t)
+        assert int(kept.item()) == int((~mref.astype(bool)).sum()), (B, t)
+        ref = xs_s.astype(np.float64) @ wd
+        if t == 1e9:
+            assert np.all(np.asarray(y) == 0)
+        else:
+            assert rel_err(y, ref) < 1e-5, (B, t, rel_err(y, ref))
