@@ -34,6 +34,13 @@
  *   teal_hist_record       <- ActivationHistogram.record (sparsifier.py:68-83)
  *   teal_hist_threshold    <- ActivationHistogram.threshold (sparsifier.py:94-117)
  *   teal_decode_attention  <- model._causal_attention, row t (model.py:135-150)
+ *   teal_gemv_batched      <- sparsifier.sparsify_batched + matmul_dense per row
+ *                             (sparsifier.py:136-155, tensor.py:130-140)
+ *   teal_output_sparse_gemv <- model.mlp_forward_output_sparse's up projection
+ *                             (model.py:331-341, the paper's CATS baseline)
+ *   teal_prefill_gate / teal_prefill_gemm <- sparsify + matmul_dense over the
+ *                             prompt rows >= sparse_from (
+ *                             the reference has no prefill)
  */
 #ifndef TEAL_B200_H
 #define TEAL_B200_H
