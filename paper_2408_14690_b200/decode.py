@@ -201,8 +201,10 @@ class SparseDecoder:
     projection's mask (dense GEMV through the same kernel)."""
 
     def __init__(self, weights: DecoderWeights, thresholds=None, kv_dtype=None, device=None,
-                 attn_chunk: int = 64, taps: bool = False):
+                 attn_chunk: int = 64, taps: bool = False, lm_threshold: float | None = None):
         self.w = weights
+        # optional LM-head input threshold (§8(f)#3): None = the dense LM head
+        self.lm_threshold = lm_threshold
         spec = self.spec = weights.spec
         dev = self.device = device or RT.require_cuda()
         self.kv_dtype = kv_dtype or weights.dtype
@@ -312,7 +314,7 @@ class SparseDecoder:
         if self.spec.vocab:
             a = C.TealGemvArgs()
             a.w_dtype, a.x_dtype, a.x, a.m, a.nseg = wcode, C.TEAL_F32, self.x.data_ptr(), d, 1
-            _seg(a, 0, W.lm_head, 0, spec.vocab, float("-inf"), self.logits)
+            _seg(a, 0, W.lm_head, 0, spec.vocab, _t32(self.lm_threshold), self.logits)
             a.prologue, a.norm_scale, a.ss_part, a.ss_count, a.eps = (
                 C.PRO_RMSNORM, W.final_norm.data_ptr(), self.ss.data_ptr(), self.ss_count, spec.norm_eps)
             a.epilogue = C.EPI_STORE

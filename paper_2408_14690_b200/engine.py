@@ -362,8 +362,11 @@ class StepDecoder:
     def __init__(self, weights, thresholds=None, kv_dtype=None, device=None,
                  taps: bool = False, attn_chunk: int = 0, ctas: int = 0,
                  count_kept: bool = False, attn_debug: bool = False, prefetch_kb: int = 0,
-                 quant: str | None = None, long_context: int = 0, long_from: int = 2048):
+                 quant: str | None = None, long_context: int = 0, long_from: int = 2048,
+                 lm_threshold: float | None = None):
         self.w = weights
+        # optional LM-head input threshold (§8(f)#3): None = the dense LM head
+        self.lm_threshold = lm_threshold
         spec = self.spec = weights.spec
         dev = self.device = device or RT.require_cuda()
         _bind()
@@ -586,7 +589,8 @@ class StepDecoder:
             mc_lm = max_contributors(nt_lm, d, Gc)
             self.ws["lm"] = torch.zeros(nt_lm * mc_lm * TW, device=dev)
             self.tk["lm"] = torch.zeros(max(4096, nt_lm), device=dev, dtype=torch.int32)
-            meta = [StepTile(float("-inf"), float("-inf"), 0, 0, 0, 0, -1, -1) for _ in range(nt_lm)]
+            t_lm = _t32(self.lm_threshold)
+            meta = [StepTile(t_lm, t_lm, 0, 0, 0, 0, -1, -1) for _ in range(nt_lm)]
             groups.append(self._group(self.lm_t, tiles_tensor(meta), m=d, n=spec.vocab, maxc=mc_lm,
                                       x=self.xv[2 * L - 1], gain=self.w.final_norm, prologue=PRO_RMS_ACC,
                                       in_acc=accs(L - 1)["down"], x_out=self.xv[2 * L], ws="lm",

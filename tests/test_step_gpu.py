@@ -270,3 +270,39 @@ def test_position_past_max_seq_raises(engine, graph):
     dec.reset(start_pos=3)
     dec.step_token()
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("engine", ["step", "launch"])
+def test_thresholded_lm_head(engine):
+    """§8(f)#3: an optional threshold on the LM head's input (the final-norm
+    row).  Logits equal where(|h| <= fl32(t), 0, h) @ W_lm of the decoder's own
+    final residual; lm_threshold None keeps the dense head."""
+    import torch
+    from paper_2408_14690_b200 import decode as D
+    from paper_2408_14690_b200 import engine as E
+    spec = D.DecoderSpec(512, 8, 2, 1024, 2, vocab=2048, rope_theta=10000.0, norm_eps=1e-5, max_seq=64)
+    W = D.random_weights(spec, torch.bfloat16, seed=9)
+    toks = [5, 77, 901, 12, 1500, 3]
+    t = 0.8
+
+    def run(lm_t):
+        dec = (E.StepDecoder if engine == "step" else D.SparseDecoder)(W, None, lm_threshold=lm_t)
+        dec.reset()
+        for tk in toks:
+            dec.token.fill_(tk)
+            dec.step_token()
+        torch.cuda.synchronize()
+        return dec
+
+    dense, sparse = run(None), run(t)
+    x = dense.x.float()
+    # the final residual row is the same in both runs (the threshold only acts on the LM head)
+    h = x / torch.sqrt((x.double() ** 2).mean().float() + spec.norm_eps) * W.final_norm
+    wl = W.lm_head.float()
+    t32 = float(np.float32(t))
+    ref_dense = h @ wl
+    ref_sparse = torch.where(h.abs() <= t32, torch.zeros_like(h), h) @ wl
+    rel = lambda a, b: float((a.double() - b.double()).norm() / b.double().norm())  # noqa: E731
+    assert rel(dense.logits, ref_dense) < 1e-4
+    assert rel(sparse.logits, ref_sparse) < 2e-3
+    assert rel(sparse.logits, ref_dense) > 1e-2  # the threshold really prunes
