@@ -330,6 +330,16 @@ int teal_batch_rope_cache(float* q, float* k, const float* v, void* k_cache, voi
 int teal_batch_silu_mul(const float* gate, const float* up, int64_t n, float* out, cudaStream_t stream);
 /* tokens[b] = argmax of logits[b] ([B][n]; lowest index on ties, NaN ignored) */
 int teal_batch_argmax(const float* logits, int B, int64_t n, int* tokens, cudaStream_t stream);
+/* Stream plumbing for running independent projections concurrently (the
+ * batch decoder's q / k / v and gate / up), in the same CUDA runtime as the
+ * library's launches: non-blocking streams, timing-free events, and
+ * teal_stream_order = record e on `signaler`, make `waiter` wait for it
+ * (graph-capture safe: the fork / join pattern). */
+int teal_stream_create(cudaStream_t* s);
+int teal_stream_destroy(cudaStream_t s);
+int teal_event_create(cudaEvent_t* e);
+int teal_event_destroy(cudaEvent_t e);
+int teal_stream_order(cudaStream_t waiter, cudaStream_t signaler, cudaEvent_t e);
 
 /* ---- persistent decode step (one launch per token) ----------------------
  *

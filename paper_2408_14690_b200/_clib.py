@@ -102,6 +102,11 @@ _SIGNATURES = [
                                              ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i64, c_vp]),
     ("teal_batch_silu_mul", ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     ("teal_batch_argmax", ctypes.c_int, [c_vp, ctypes.c_int, c_i64, c_vp, c_vp]),
+    ("teal_stream_create", ctypes.c_int, [ctypes.POINTER(c_vp)]),
+    ("teal_stream_destroy", ctypes.c_int, [c_vp]),
+    ("teal_event_create", ctypes.c_int, [ctypes.POINTER(c_vp)]),
+    ("teal_event_destroy", ctypes.c_int, [c_vp]),
+    ("teal_stream_order", ctypes.c_int, [c_vp, c_vp, c_vp]),
     ("teal_residual_add", ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, ctypes.c_int, c_vp]),
     ("teal_step_ctas_per_sm", ctypes.c_int, [ctypes.c_int]),
     ("teal_gemv_batched_workspace", ctypes.c_int, [ctypes.POINTER(TealGemvBatchedArgs), ctypes.POINTER(ctypes.c_int),

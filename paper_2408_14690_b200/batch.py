@@ -61,7 +61,7 @@ class BatchDecoder:
     saw, the shared masks and a few intermediates (tests / calibration)."""
 
     def __init__(self, weights: DecoderWeights, thresholds, batch: int, quant: str | None = None,
-                 kv_dtype=None, taps: bool = False, count_kept: bool = False):
+                 kv_dtype=None, taps: bool = False, count_kept: bool = False, concurrent: bool = True):
         spec = self.spec = weights.spec
         if not spec.vocab:
             raise ValueError("BatchDecoder needs an embedding and LM head (vocab > 0)")
@@ -124,6 +124,17 @@ class BatchDecoder:
             self.tap_down = torch.zeros(L, B, d, **f32)         # down projection output
             self.tap_final = torch.zeros(B, d, **f32)           # final-norm LM-head input
             self.masks = {p: torch.zeros(L, spec.proj_shapes()[p][1], device=dev, dtype=torch.uint8) for p in PROJ}
+        # q / k / v (and gate / up) read the same input with their own masks:
+        # with `concurrent` they run on three (two) streams at once, each launch
+        # on its share of the SMs, so their fixed costs overlap
+        self.concurrent = concurrent
+        self._side, self._ev = [], []
+        if concurrent:
+            for lst, fn in ((self._side, "teal_stream_create"), (self._ev, "teal_event_create")):
+                for _ in range(2 if lst is self._side else 3):
+                    h = ctypes.c_void_p()
+                    C.call(fn, ctypes.byref(h))
+                    lst.append(h.value)
         self._build_args()
         self.graph = None
         self._pos = 0
@@ -142,6 +153,32 @@ class BatchDecoder:
         self._tk_need = max(self._tk_need, ntk.value)
         return a
 
+    def _resize(self, a):
+        g, nws, ntk = ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
+        C.call("teal_gemv_batched_workspace", ctypes.byref(a), ctypes.byref(g), ctypes.byref(nws), ctypes.byref(ntk))
+        self._ws_need = max(self._ws_need, nws.value)
+        self._tk_need = max(self._tk_need, ntk.value)
+        return a
+
+    def _fork(self, sh: int, n: int) -> list:
+        """Side streams that start after everything issued on `sh` so far."""
+        for st in self._side[:n]:
+            C.call("teal_stream_order", st, sh, self._ev[0])
+        return self._side[:n]
+
+    def _join(self, sh: int, n: int) -> None:
+        for i, st in enumerate(self._side[:n]):
+            C.call("teal_stream_order", sh, st, self._ev[1 + i])
+
+    def __del__(self):
+        try:
+            for st in getattr(self, "_side", []):
+                C.lib().teal_stream_destroy(st)
+            for ev in getattr(self, "_ev", []):
+                C.lib().teal_event_destroy(ev)
+        except Exception:
+            pass
+
     def _build_args(self):
         self._ws_need, self._tk_need = 1, 1
         L = self.spec.n_layers
@@ -158,12 +195,21 @@ class BatchDecoder:
                 row[p] = self._gemv_args(self.pw[l][p], inputs[p], outputs[p], self.thresholds[l][i], mask, kept)
             self.args.append(row)
         self.lm_args = self._gemv_args(self.lm, self.h, self.logits, None)
-        self.ws = torch.zeros(self._ws_need, device=self.device)
-        self.tk = torch.zeros(self._tk_need, device=self.device, dtype=torch.int32)
+        if self.concurrent:  # SM shares of the concurrent launches (workspace sized after)
+            sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+            share = {"q": sms, "k": sms // 2, "v": sms // 2, "gate": 0, "up": 0}
+            for l, row in enumerate(self.args):
+                for p_, c in share.items():
+                    row[p_].ctas = c
+                    row[p_] = self._resize(row[p_])
+        # concurrent launches need their own workspace: one per projection slot
+        # (layers run in order, so the slots are reused across layers)
+        self.ws = {p_: torch.zeros(self._ws_need, device=self.device) for p_ in PROJ}
+        self.tk = {p_: torch.zeros(self._tk_need, device=self.device, dtype=torch.int32) for p_ in PROJ}
         for row in self.args:
-            for a in row.values():
-                a.ws, a.tickets = self.ws.data_ptr(), self.tk.data_ptr()
-        self.lm_args.ws, self.lm_args.tickets = self.ws.data_ptr(), self.tk.data_ptr()
+            for p_, a in row.items():
+                a.ws, a.tickets = self.ws[p_].data_ptr(), self.tk[p_].data_ptr()
+        self.lm_args.ws, self.lm_args.tickets = self.ws["q"].data_ptr(), self.tk["q"].data_ptr()
 
     # -- step ---------------------------------------------------------------------
     def reset(self, start_pos: int = 0) -> None:
@@ -182,8 +228,8 @@ class BatchDecoder:
         d, f, hd, H, KVH = sp.d_model, sp.d_ff, sp.head_dim, sp.n_heads, sp.n_kv_heads
         T = self.taps
 
-        def gemv(a):
-            C.check(Lb.teal_gemv_batched(ctypes.byref(a), sh))
+        def gemv(a, stream=None):
+            C.check(Lb.teal_gemv_batched(ctypes.byref(a), sh if stream is None else stream))
 
         C.check(Lb.teal_batch_embed(self.w.embedding.data_ptr(), RT.dtype_code(self.w.embedding.dtype),
                                     self.tokens.data_ptr(), B, d, self.x.data_ptr(), self.state.data_ptr(), sh))
@@ -195,9 +241,16 @@ class BatchDecoder:
                                           self.h.data_ptr(), sh))
             if T is not None:
                 T["pre_attn"][l].copy_(self.h)
-            gemv(A["q"])
-            gemv(A["k"])
-            gemv(A["v"])
+            if self.concurrent:
+                s1, s2 = self._fork(sh, 2)
+                gemv(A["k"], s1)
+                gemv(A["v"], s2)
+                gemv(A["q"])
+                self._join(sh, 2)
+            else:
+                gemv(A["q"])
+                gemv(A["k"])
+                gemv(A["v"])
             C.check(Lb.teal_batch_rope_cache(self.q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(),
                                              self.kcache[l].data_ptr(), self.vcache[l].data_ptr(),
                                              RT.dtype_code(self.kv_dtype), RT.ptr(self.rope_cos),
@@ -218,8 +271,14 @@ class BatchDecoder:
                                           sp.norm_eps, B, d, self.h.data_ptr(), sh))
             if T is not None:
                 T["pre_mlp"][l].copy_(self.h)
-            gemv(A["gate"])
-            gemv(A["up"])
+            if self.concurrent:
+                (s1,) = self._fork(sh, 1)
+                gemv(A["up"], s1)
+                gemv(A["gate"])
+                self._join(sh, 1)
+            else:
+                gemv(A["gate"])
+                gemv(A["up"])
             C.check(Lb.teal_batch_silu_mul(self.gate.data_ptr(), self.up.data_ptr(), B * f, self.inter.data_ptr(), sh))
             if T is not None:
                 T["mlp_inter"][l].copy_(self.inter)

@@ -220,4 +220,30 @@ int teal_batch_argmax(const float* logits, int B, int64_t n, int* tokens, cudaSt
     return check_launch("teal_batch_argmax");
 }
 
+// ---- stream ordering for concurrent projections (same runtime as the launches) ----
+int teal_stream_create(cudaStream_t* s) {
+    TEAL_REQUIRE(s, "teal_stream_create: null pointer");
+    if (cudaStreamCreateWithFlags(s, cudaStreamNonBlocking) != cudaSuccess) return check_launch("teal_stream_create");
+    return TEAL_OK;
+}
+int teal_stream_destroy(cudaStream_t s) {
+    cudaStreamDestroy(s);
+    return check_launch("teal_stream_destroy");
+}
+int teal_event_create(cudaEvent_t* e) {
+    TEAL_REQUIRE(e, "teal_event_create: null pointer");
+    if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return check_launch("teal_event_create");
+    return TEAL_OK;
+}
+int teal_event_destroy(cudaEvent_t e) {
+    cudaEventDestroy(e);
+    return check_launch("teal_event_destroy");
+}
+int teal_stream_order(cudaStream_t waiter, cudaStream_t signaler, cudaEvent_t e) {
+    TEAL_REQUIRE(e, "teal_stream_order: null event");
+    if (cudaEventRecord(e, signaler) != cudaSuccess || cudaStreamWaitEvent(waiter, e, 0) != cudaSuccess)
+        return check_launch("teal_stream_order");
+    return TEAL_OK;
+}
+
 }  // extern "C"
