@@ -143,8 +143,28 @@ __device__ __forceinline__ void wait_range_sys(const int* counters, int c0, int 
     __syncthreads();
 }
 
-// thread 0 polls with backoff; the barrier publishes the result to the CTA
+#ifndef TEAL_PAR_WAIT
+#define TEAL_PAR_WAIT 1
+#endif
+// warp 0 polls up to 32 counters at once (one L2 round trip for a row range
+// spanning several producer tiles, not one per counter), with backoff; the
+// barrier publishes the result to the CTA
 __device__ __forceinline__ void wait_range(const int* counters, int c0, int c1, int target) {
+#if TEAL_PAR_WAIT
+    if (threadIdx.x < 32) {
+        for (int b = c0; b <= c1; b += 32) {
+            const int c = b + (int)threadIdx.x;
+            const int* p = counters + (int64_t)c * CSTRIDE;
+            bool done = c > c1 || ld_acquire(p) >= target;
+            unsigned ns = 32;
+            while (!__all_sync(0xffffffffu, done)) {
+                __nanosleep(ns);
+                ns = ns < TEAL_POLL_NS ? ns * 2 : TEAL_POLL_NS;
+                if (!done) done = ld_acquire(p) >= target;
+            }
+        }
+    }
+#else
     if (threadIdx.x == 0) {
         for (int c = c0; c <= c1; ++c) {
             unsigned ns = 32;
@@ -154,6 +174,7 @@ __device__ __forceinline__ void wait_range(const int* counters, int c0, int c1, 
             }
         }
     }
+#endif
     __syncthreads();
 }
 
