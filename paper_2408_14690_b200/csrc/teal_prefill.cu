@@ -57,11 +57,11 @@ constexpr int UK = 16;   // UMMA K for kind::f16
 #define PF_A_SBO 1024    // A: byte stride between 8-input-row groups
 #endif
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int NBT = 1>
 struct Cfg {
     static constexpr int A_BYTES = BK * BM * 2;  // 16 KB: 64 input rows x 128 outputs
     static constexpr int B_BYTES = BN * BK * 2;  // BN tokens x 64 inputs
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGE_BYTES = A_BYTES + NBT * B_BYTES;  // NBT activation tiles share the weight tile
     static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
     static constexpr uint32_t TMEM_COLS = 2u * BN;  // double-buffered accumulator (power of 2)
     // kind::f16 instruction descriptor: D f32, A / B bf16, A MN-major, B K-major, N, M
@@ -117,13 +117,17 @@ struct Shape {
     int n_tiles, t_tiles, splits, kps, m_blocks, accumulate;
 };
 
-// persistent: CTA c runs units c, c + G, ...; unit = (output tile i, token tile j, K split sp)
-template <int BN, int TERMS, int STAGES>
+// persistent: CTA c runs units c, c + G, ...; unit = (output tile i, token tile j, K split sp).
+// SHARE: one stage holds the weight tile and every term's activation tile (the weight
+// tile is staged once per K block); otherwise each term is its own stage.
+template <int BN, int TERMS, int STAGES, bool SHARE = false>
 __global__ void __launch_bounds__(NT, 1)
 prefill_gemm_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap txh,
                     const __grid_constant__ CUtensorMap txl, const Shape sh, float* __restrict__ y,
                     float* __restrict__ ws, uint32_t* __restrict__ tickets) {
-    using C = Cfg<BN, STAGES>;
+    using C = Cfg<BN, STAGES, SHARE ? TERMS : 1>;
+    constexpr int NV = SHARE ? 1 : TERMS;   // stages per K block
+    constexpr int NBT = SHARE ? TERMS : 1;  // activation tiles per stage
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
@@ -169,14 +173,16 @@ prefill_gemm_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constan
                 const int kb0 = sp * sh.kps, kb1 = min(sh.m_blocks, kb0 + sh.kps);
                 for (int kb = kb0; kb < kb1; ++kb) {
 #pragma unroll
-                    for (int term = 0; term < TERMS; ++term, ++it) {
+                    for (int v = 0; v < NV; ++v, ++it) {
                         const uint32_t s = it % STAGES;
                         if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
                         uint8_t* st = smem + s * C::STAGE_BYTES;
                         mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
                         tma_2d(st, &tw, i * BM, kb * BK, &full[s]);
                         tma_2d(st + C::A_BYTES / 2, &tw, i * BM + BM / 2, kb * BK, &full[s]);
-                        tma_2d(st + C::A_BYTES, term ? &txl : &txh, kb * BK, j * BN, &full[s]);
+#pragma unroll
+                        for (int b = 0; b < NBT; ++b)
+                            tma_2d(st + C::A_BYTES + b * C::B_BYTES, (v + b) ? &txl : &txh, kb * BK, j * BN, &full[s]);
                     }
                 }
             }
@@ -194,7 +200,7 @@ prefill_gemm_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constan
                 uint32_t acc = 0;
                 for (int kb = kb0; kb < kb1; ++kb) {
 #pragma unroll
-                    for (int term = 0; term < TERMS; ++term, ++it) {
+                    for (int v = 0; v < NV; ++v, ++it) {
                         const uint32_t s = it % STAGES;
                         mbar_wait(&full[s], (it / STAGES) & 1);
                         tc_fence_after();
@@ -203,9 +209,12 @@ prefill_gemm_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constan
 #pragma unroll
                         for (int kk = 0; kk < BK / UK; ++kk) {
                             // A: 16 input rows = 2 swizzle atoms of 8 rows x 128 B; B: 16 bf16 = 32 B along the swizzled row
-                            tc_mma(d, sw128_desc(a0 + kk * UK * 128, PF_A_LBO, PF_A_SBO),
-                                   sw128_desc(b0 + kk * UK * 2, 16, 1024), C::IDESC, acc);
-                            acc = 1u;
+                            const uint64_t ad = sw128_desc(a0 + kk * UK * 128, PF_A_LBO, PF_A_SBO);
+#pragma unroll
+                            for (int b = 0; b < NBT; ++b) {
+                                tc_mma(d, ad, sw128_desc(b0 + b * C::B_BYTES + kk * UK * 2, 16, 1024), C::IDESC, acc);
+                                acc = 1u;
+                            }
                         }
                         tc_commit(&empty[s]);  // the stage is free once these MMAs have read it
                     }
@@ -436,9 +445,9 @@ Shape plan(const teal_prefill_args* a) {
     return sh;
 }
 
-template <int BN, int TERMS, int STAGES>
+template <int BN, int TERMS, int STAGES, bool SHARE = false>
 int launch(const teal_prefill_args* a, const Shape& sh, cudaStream_t stream) {
-    using C = Cfg<BN, STAGES>;
+    using C = Cfg<BN, STAGES, SHARE ? TERMS : 1>;
     CUtensorMap tw, txh, txl;
     int rc = make_map(&tw, a->w, a->n, a->m, a->ldw, BK);
     if (rc) return rc;
@@ -453,7 +462,8 @@ int launch(const teal_prefill_args* a, const Shape& sh, cudaStream_t stream) {
     if (cudaGetDevice(&dev) != cudaSuccess) return check_launch("teal_prefill_gemm (device)");
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(__atomic_load_n(&attr, __ATOMIC_ACQUIRE) & bit)) {
-        cudaFuncSetAttribute(prefill_gemm_kernel<BN, TERMS, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(prefill_gemm_kernel<BN, TERMS, STAGES, SHARE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM);
         __atomic_fetch_or(&attr, bit, __ATOMIC_RELEASE);
     }
     const int units = sh.n_tiles * sh.t_tiles * sh.splits;
@@ -467,7 +477,7 @@ int launch(const teal_prefill_args* a, const Shape& sh, cudaStream_t stream) {
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = sh.splits > 1 ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, prefill_gemm_kernel<BN, TERMS, STAGES>, tw, txh, txl, sh, a->y, a->ws, a->tickets);
+    cudaLaunchKernelEx(&cfg, prefill_gemm_kernel<BN, TERMS, STAGES, SHARE>, tw, txh, txl, sh, a->y, a->ws, a->tickets);
     return check_launch("teal_prefill_gemm");
 }
 
@@ -529,7 +539,12 @@ int teal_prefill_gemm(const teal_prefill_args* a, cudaStream_t stream) {
         sh = plan(&one);
     }
     const bool two = a->x_lo != nullptr;
-    if (bn_for(a->T, a->n) == 128) return two ? launch<128, 2, 6>(a, sh, stream) : launch<128, 1, 6>(a, sh, stream);
+    // two terms: at BN = 128 one stage carries the weight tile and both activation
+    // tiles (4 stages; the weight tile staged once: q/o T = 512 43.9 -> 37.4 us); at
+    // BN = 256 that leaves 2 stages, too shallow (gate/up T = 2048 341 -> 409 us),
+    // so each term keeps its own stage there
+    if (bn_for(a->T, a->n) == 128)
+        return two ? launch<128, 2, 4, true>(a, sh, stream) : launch<128, 1, 6>(a, sh, stream);
     return two ? launch<256, 2, 4>(a, sh, stream) : launch<256, 1, 4>(a, sh, stream);
 }
 
