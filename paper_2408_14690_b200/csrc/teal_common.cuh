@@ -13,7 +13,7 @@ constexpr int kWarps = kThreads / 32;
 
 // ---- error reporting (thread-local message, no exceptions across the ABI) --
 void set_error(const char* fmt, ...);
-int pdl_enabled();  // TEAL_PDL=0 disables programmatic dependent launch
+int pdl_enabled();  // programmatic dependent launch between the library's consecutive launches
 int check_launch(const char* what);
 
 #define TEAL_REQUIRE(cond, ...)            \
