@@ -123,3 +123,55 @@ def test_cli_bench_tsv(tmp_path):
     lines = out.read_text().splitlines()
     assert lines[0].split("\t") == ["sparsity", "median_ns", "min_ns", "dense_median_ns", "speedup", "weight_bytes"]
     assert len(lines) == 3 and (tmp_path / "bench.tsv.manifest.json").exists()
+
+
+def test_prefill_workspace_plan_and_validation():
+    """teal_prefill_workspace (host planning, no GPU): K splits only below the
+    SM count, ws = splits * T * n floats, two tickets per output tile; shape
+    checks raise the reference's ValueError."""
+    import ctypes
+    from paper_2408_14690_b200 import _clib as C
+
+    def plan(T, m, n, splits=0):
+        a = C.TealPrefillArgs(m=m, n=n, ldw=n, T=T, ldx=m, ldy=n, splits=splits)
+        ns, wsf, tks = ctypes.c_int(0), C.c_i64(0), C.c_i64(0)
+        C.call("teal_prefill_workspace", ctypes.byref(a), ctypes.byref(ns), ctypes.byref(wsf), ctypes.byref(tks))
+        return ns.value, wsf.value, tks.value
+
+    s, ws, tk = plan(2048, 4096, 14336)          # 112 x 8 tiles >= SMs: no split
+    assert s == 1 and ws == 0 and tk == 0
+    s, ws, tk = plan(128, 4096, 1024)            # 8 tiles: split K
+    assert s > 1 and ws == s * 128 * 1024 and tk == 2 * 8
+    assert plan(128, 4096, 1024, splits=1)[0] == 1
+    assert plan(100, 4096, 4096, splits=3)[0] == 3
+    with pytest.raises(ValueError, match="multiple of 64"):
+        plan(16, 96, 128)
+    from paper_2408_14690_b200 import prefill as P
+    import torch
+    with pytest.raises(ValueError, match="non-negative"):
+        P.gate(torch.zeros(2, 64), -0.5)
+    with pytest.raises(ValueError, match="sparse_from"):
+        P.gate(torch.zeros(2, 64), 0.5, sparse_from=-1)
+    with pytest.raises(ValueError, match="terms"):
+        P.gate(torch.zeros(2, 64), 0.5, terms=3)
+
+
+def test_batched_route_plan():
+    """teal_gemv_batched_workspace picks the tcgen05 route (ctas reported 0,
+    compaction + operand workspace) for bf16, B >= 4, n >= 8192, and the
+    mma.sync / FMA kernels otherwise."""
+    import ctypes
+    from paper_2408_14690_b200 import _clib as C
+
+    def route(B, m, n, wdt=C.TEAL_BF16):
+        a = C.TealGemvBatchedArgs(m=m, n=n, ldw=n, w_dtype=wdt, B=B, group=128, t32=0.5)
+        a.w, a.x, a.y, a.scale = 16, 16, 16, 16   # validation needs non-null pointers; nothing is launched
+        g, nws, ntk = ctypes.c_int(-1), ctypes.c_int64(0), ctypes.c_int64(0)
+        C.call("teal_gemv_batched_workspace", ctypes.byref(a), ctypes.byref(g), ctypes.byref(nws), ctypes.byref(ntk))
+        return g.value, nws.value, ntk.value
+
+    g, nws, ntk = route(16, 4096, 14336)
+    assert g == 0 and nws > 16 * 4096 and ntk == 14336 // 128      # tcgen05: operand tiles, kept lists, counts
+    assert route(16, 4096, 4096)[0] > 0                              # narrow: mma.sync
+    assert route(2, 4096, 14336)[0] > 0                              # B < 4: FMA kernel
+    assert route(16, 4096, 14336, C.TEAL_I8)[0] > 0                  # int8: mma.sync
