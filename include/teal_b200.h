@@ -177,7 +177,13 @@ int teal_dense_gemv(const void* w, int w_dtype, int64_t m, int64_t n, int64_t ld
  * (sparsifier.py:136-155, tensor.py:130-140) for B <= 16 decode rows:
  * column i is pruned in every row iff mean_b |x[b,i]| <= t32 (fp32 sum in
  * ascending b, fp64 quotient rounded to fp32), and
- * y[b] = sum over kept i of x[b,i] * W[i,:] — each kept row read once. */
+ * y[b] = sum over kept i of x[b,i] * W[i,:] — each kept row read once.
+ * Routes: bf16 rows, 4 <= B <= 16, n a multiple of 128 with n >= 8192 (and a
+ * 16-byte aligned w): a compaction launch + a tcgen05 / TMEM contraction
+ * (teal_gemv_tc.cu; ctas is ignored and reported 0 by the workspace query;
+ * ws must be 256-byte aligned); other shapes at B >= 4: the mma.sync kernel;
+ * B < 4: the CUDA-core kernel.  All routes give the same mask and kept count
+ * and the fp32-GEMV accuracy. */
 typedef struct teal_gemv_batched_args {
     const void* w;               /* input-major rows, row stride ldw elements   */
     const float* scale;          /* I8: [n]; I4: [ceil(m/group)][n]             */
