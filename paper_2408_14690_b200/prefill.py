@@ -156,24 +156,30 @@ class SparsePrefill:
         else:
             self.rope_cos = self.rope_sin = None
 
-    def _attend(self, q, kc, vc, T):
-        """Causal attention of the prompt rows over the cached (kv-dtype) keys
-        and values: fp32 (fused memory-efficient kernel; the decode engine's
-        arithmetic: fp32 q, fp32 softmax) or bf16 (flash kernel, q rounded)."""
+    def _attend(self, q, kc, vc, T, pos0=0):
+        """Causal attention of the prompt rows (positions pos0 .. pos0+T-1) over
+        the cached (kv-dtype) keys and values of positions 0 .. pos0+T-1: fp32
+        (fused memory-efficient kernel; the decode engine's arithmetic: fp32 q,
+        fp32 softmax) or bf16 (flash kernel, q rounded)."""
         from torch.nn.attention import SDPBackend, sdpa_kernel
         spec = self.spec
         G, hd = spec.n_heads // spec.n_kv_heads, spec.head_dim
+        S = pos0 + T
         qh = q.view(T, spec.n_heads, hd).transpose(0, 1).unsqueeze(0)
+        mask = None
+        if pos0:  # key j visible to row t iff j <= pos0 + t
+            mask = (torch.arange(S, device=q.device)[None, :] <= (pos0 + torch.arange(T, device=q.device))[:, None])
+        kw = dict(is_causal=True) if mask is None else dict(attn_mask=mask)
         if self.attention == "fp32":
-            kk = kc[:, :T].float().repeat_interleave(G, dim=0).unsqueeze(0)
-            vv = vc[:, :T].float().repeat_interleave(G, dim=0).unsqueeze(0)
+            kk = kc[:, :S].float().repeat_interleave(G, dim=0).unsqueeze(0)
+            vv = vc[:, :S].float().repeat_interleave(G, dim=0).unsqueeze(0)
             with sdpa_kernel([SDPBackend.EFFICIENT_ATTENTION, SDPBackend.MATH]):
-                ctx = torch.nn.functional.scaled_dot_product_attention(qh, kk, vv, is_causal=True)
+                ctx = torch.nn.functional.scaled_dot_product_attention(qh, kk, vv, **kw)
         else:
-            kk = kc[:, :T].to(torch.bfloat16).repeat_interleave(G, dim=0).unsqueeze(0)
-            vv = vc[:, :T].to(torch.bfloat16).repeat_interleave(G, dim=0).unsqueeze(0)
+            kk = kc[:, :S].to(torch.bfloat16).repeat_interleave(G, dim=0).unsqueeze(0)
+            vv = vc[:, :S].to(torch.bfloat16).repeat_interleave(G, dim=0).unsqueeze(0)
             with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION, SDPBackend.MATH]):
-                ctx = torch.nn.functional.scaled_dot_product_attention(qh.to(torch.bfloat16), kk, vv, is_causal=True)
+                ctx = torch.nn.functional.scaled_dot_product_attention(qh.to(torch.bfloat16), kk, vv, **kw)
         return ctx[0].transpose(0, 1).reshape(T, spec.n_q).float().contiguous()
 
     # one projection: y (+)= g(x) @ w[:, c0:c0+n]
@@ -185,11 +191,14 @@ class SparsePrefill:
         return gemm(w, hi, lo, out=out, accumulate=accumulate)
 
     def forward(self, tokens=None, hidden=None, sparse_from: int | None = None, decoder=None, logits: str = "last",
-                kv_cache=None) -> PrefillResult:
+                kv_cache=None, start_pos: int = 0) -> PrefillResult:
         """Run the prompt (``tokens`` [T] int, or ``hidden`` rows [T, d]).
-        ``sparse_from`` default T // 2.  ``logits``: "last", "all" or "none".
-        ``kv_cache``: (k, v) tensors [L, KVH, max_seq, hd] to fill (default:
-        the decoder's, else fresh ones)."""
+        ``sparse_from`` default T // 2 (rows of THIS call).  ``logits``:
+        "last", "all" or "none".  ``kv_cache``: (k, v) tensors [L, KVH,
+        max_seq, hd] to fill (default: the decoder's, else fresh ones).
+        ``start_pos`` > 0: chunked prefill — the rows are positions start_pos ..
+        start_pos+T-1 and attend to the cache's earlier positions (filled by a
+        previous call on the same cache)."""
         spec, W = self.spec, self.w
         d, f, nq, nkv, hd = spec.d_model, spec.d_ff, spec.n_q, spec.n_kv, spec.head_dim
         dev = W.layers[0].wqkv.device
@@ -210,8 +219,9 @@ class SparsePrefill:
                 __import__("numpy").ascontiguousarray(hidden, dtype="float32"))
             x = h0.to(dev, torch.float32).reshape(-1, d).clone()
             T = x.shape[0]
-        if T < 1 or T > spec.max_seq:
-            raise ValueError(f"prompt length {T} outside [1, max_seq={spec.max_seq}]")
+        pos0 = int(start_pos)
+        if T < 1 or pos0 < 0 or pos0 + T > spec.max_seq:
+            raise ValueError(f"prompt positions [{pos0}, {pos0 + T}) outside [0, max_seq={spec.max_seq})")
         sf = T // 2 if sparse_from is None else int(sparse_from)
         if sf < 0:
             raise ValueError(f"sparse_from must be >= 0, got {sf}")
@@ -220,6 +230,8 @@ class SparsePrefill:
         elif decoder is not None:
             kc_all, vc_all = decoder.kcache, decoder.vcache
         else:
+            if pos0:
+                raise ValueError("start_pos > 0 continues a cache: pass kv_cache or decoder")
             kc_all = torch.zeros(spec.n_layers, spec.n_kv_heads, spec.max_seq, hd, device=dev, dtype=self.kv_dtype)
             vc_all = torch.zeros_like(kc_all)
         kvc = RT.dtype_code(kc_all.dtype)
@@ -240,10 +252,10 @@ class SparsePrefill:
             self._proj(h, lw.wqkv[:, nq + nkv:], t[2], sf, out=v, kept=kept[l, 2])
             kc, vc = kc_all[l], vc_all[l]
             C.check(L.teal_prefill_rope_cache(q.data_ptr(), nq, k.data_ptr(), nkv, v.data_ptr(), nkv, T,
-                                              spec.n_heads, spec.n_kv_heads, hd, 0, RT.ptr(self.rope_cos),
+                                              spec.n_heads, spec.n_kv_heads, hd, pos0, RT.ptr(self.rope_cos),
                                               RT.ptr(self.rope_sin), kc.data_ptr(), vc.data_ptr(), kvc,
                                               spec.max_seq, sh))
-            ctx = self._attend(q, kc, vc, T)
+            ctx = self._attend(q, kc, vc, T, pos0)
             self._proj(ctx, lw.wo, t[3], sf, out=x, accumulate=True, kept=kept[l, 3])
             C.check(L.teal_batch_rmsnorm(x.data_ptr(), None, lw.rms_mlp.data_ptr(), spec.norm_eps, T, d,
                                          h.data_ptr(), sh))
@@ -262,7 +274,7 @@ class SparsePrefill:
             C.check(L.teal_batch_argmax(lg.data_ptr(), lg.shape[0], lg.shape[1], toks.data_ptr(), sh))
             nxt = toks[-1:]
         if decoder is not None:
-            decoder.reset(T)
+            decoder.reset(pos0 + T)
             if nxt is not None:
                 decoder.token.copy_(nxt)
         return PrefillResult(x, lg, nxt, kept)

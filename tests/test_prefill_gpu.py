@@ -224,3 +224,26 @@ def test_prefill_dense_prefix_matches_reference_forward(P):
         want = T.model_forward_sparse(mr, X, cfgs, dense_prefix=k) if k else T.model_forward_sparse(mr, X, cfgs)
         got = P.SparsePrefill(W, thr, kv_dtype=torch.float32).forward(hidden=X, sparse_from=k).x
         assert rel_err(got, torch.as_tensor(want).to(got.device)) < 1e-5, k
+
+
+def test_chunked_prefill_equals_one_pass(P):
+    # the prompt in two chunks (the second attends to the first's cached K/V,
+    # RoPE at its absolute positions) == one pass over the whole prompt
+    W = _llama_toy(seed=5)
+    from paper_2408_14690_b200 import decode as D
+    thr = D.calibrate_thresholds(W, 0.5, n_tokens=16, engine="launch")
+    toks = torch.randint(0, 1024, (56,), generator=torch.Generator().manual_seed(4))
+    pf = P.SparsePrefill(W, thr, kv_dtype=torch.float32)
+    L_, KVH, S, hd = W.spec.n_layers, W.spec.n_kv_heads, W.spec.max_seq, W.spec.head_dim
+    one = (torch.zeros(L_, KVH, S, hd, device="cuda"), torch.zeros(L_, KVH, S, hd, device="cuda"))
+    two = (torch.zeros_like(one[0]), torch.zeros_like(one[1]))
+    r1 = pf.forward(tokens=toks, sparse_from=0, kv_cache=one, logits="all")
+    pf.forward(tokens=toks[:24], sparse_from=0, kv_cache=two, logits="none")
+    r2 = pf.forward(tokens=toks[24:], sparse_from=0, kv_cache=two, logits="all", start_pos=24)
+    T = len(toks)
+    assert rel_err(two[0][:, :, :T], one[0][:, :, :T]) < 1e-5
+    assert rel_err(two[1][:, :, :T], one[1][:, :, :T]) < 1e-5
+    assert rel_err(r2.x, r1.x[24:]) < 1e-5
+    assert torch.equal(r2.next_token, r1.next_token)
+    with pytest.raises(ValueError, match="continues a cache"):
+        pf.forward(tokens=toks[:4], start_pos=4)
