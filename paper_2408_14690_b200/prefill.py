@@ -278,3 +278,22 @@ class SparsePrefill:
             if nxt is not None:
                 decoder.token.copy_(nxt)
         return PrefillResult(x, lg, nxt, kept)
+
+    def forward_batch(self, prompts, batch_decoder, sparse_from: int | None = None) -> list:
+        """Prefill the B equal-length prompts of a small-batch decode: prompt b
+        fills sequence b's slice of ``batch_decoder``'s cache (per-token masks,
+        as in the prompt pass), then the batch decoder continues in lockstep at
+        position T from each prompt's argmax token.  Returns the B results."""
+        B = batch_decoder.B
+        if len(prompts) != B or len({len(p_) for p_ in prompts}) != 1:
+            raise ValueError(f"need {B} prompts of one length (the batch decodes in lockstep)")
+        out = []
+        for b, pr in enumerate(prompts):
+            r = self.forward(tokens=pr, sparse_from=sparse_from,
+                             kv_cache=(batch_decoder.kcache[:, b], batch_decoder.vcache[:, b]))
+            out.append(r)
+        T = len(prompts[0])
+        batch_decoder.reset(T)
+        if out[0].next_token is not None:
+            batch_decoder.tokens.copy_(torch.cat([r.next_token for r in out]))
+        return out

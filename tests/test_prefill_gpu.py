@@ -247,3 +247,26 @@ def test_chunked_prefill_equals_one_pass(P):
     assert torch.equal(r2.next_token, r1.next_token)
     with pytest.raises(ValueError, match="continues a cache"):
         pf.forward(tokens=toks[:4], start_pos=4)
+
+
+def test_batch_prefill_hands_off_to_the_batch_decoder(P):
+    # B prompts prefilled into the batch decoder's per-sequence cache slices,
+    # then one lockstep step == the batch decoder stepped through the prompts
+    # (dense: the per-token and the shared batch masks coincide)
+    from paper_2408_14690_b200 import batch as BT
+    W = _llama_toy(seed=6)
+    B, T = 4, 20
+    prompts = torch.randint(0, 1024, (B, T), generator=torch.Generator().manual_seed(8))
+    ref = BT.BatchDecoder(W, None, B)
+    ref.reset()
+    for t in range(T):
+        ref.tokens.copy_(prompts[:, t].to(torch.int32))
+        ref.step()
+    ref_next = ref.tokens.clone()
+    ref.step()
+    dec = BT.BatchDecoder(W, None, B)
+    dec.reset()
+    P.SparsePrefill(W, None).forward_batch([p_.tolist() for p_ in prompts], dec)
+    assert torch.equal(dec.tokens, ref_next)
+    dec.step()
+    assert rel_err(dec.logits, ref.logits) < 1e-3  # bf16 caches: one-ulp rounding differences
