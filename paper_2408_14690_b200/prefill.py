@@ -297,3 +297,26 @@ class SparsePrefill:
         if out[0].next_token is not None:
             batch_decoder.tokens.copy_(torch.cat([r.next_token for r in out]))
         return out
+
+
+def generate(weights, thresholds, prompt, max_new_tokens: int, sparse_from: int | None = None, kv_dtype=None,
+             prefill_thresholds="same") -> list:
+    """Greedy generation: the prompt through ``SparsePrefill`` (``sparse_from``
+    default: the second half; ``prefill_thresholds`` "same"
+    or None for a dense prompt pass — the paper does not sparsify prefill on
+    generation tasks), then ``max_new_tokens`` steps of the persistent decode
+    engine (one CUDA-graph replay per token) continuing the same KV cache.
+    Returns the generated token ids."""
+    from . import engine as E
+    dec = E.StepDecoder(weights, thresholds, kv_dtype=kv_dtype)
+    dec.reset()
+    pthr = thresholds if prefill_thresholds == "same" else prefill_thresholds
+    r = SparsePrefill(weights, pthr, kv_dtype=dec.kv_dtype).forward(tokens=prompt, sparse_from=sparse_from,
+                                                                   decoder=dec)
+    out = [int(r.next_token)]
+    if max_new_tokens > 1:
+        dec.capture()
+        for _ in range(max_new_tokens - 1):
+            dec.step_token()
+            out.append(int(dec.token))
+    return out[:max_new_tokens]

@@ -270,3 +270,22 @@ def test_batch_prefill_hands_off_to_the_batch_decoder(P):
     assert torch.equal(dec.tokens, ref_next)
     dec.step()
     assert rel_err(dec.logits, ref.logits) < 1e-3  # bf16 caches: one-ulp rounding differences
+
+
+def test_generate_matches_step_decoding(P):
+    # prefill + graph-replayed decode == the step engine stepped through the
+    # prompt and then decoding greedily (dense, fp32 caches: no rounding ties)
+    from paper_2408_14690_b200 import engine as E
+    W = _llama_toy(seed=7)
+    prompt = torch.randint(0, 1024, (16,), generator=torch.Generator().manual_seed(9)).tolist()
+    got = P.generate(W, None, prompt, 8, kv_dtype=torch.float32)
+    dec = E.StepDecoder(W, None, kv_dtype=torch.float32)
+    dec.reset()
+    for t in prompt:
+        dec.token.fill_(t)
+        dec.step_token()
+    want = [int(dec.token)]
+    for _ in range(7):
+        dec.step_token()
+        want.append(int(dec.token))
+    assert got == want
