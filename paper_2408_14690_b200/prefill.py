@@ -320,3 +320,18 @@ def generate(weights, thresholds, prompt, max_new_tokens: int, sparse_from: int 
             dec.step_token()
             out.append(int(dec.token))
     return out[:max_new_tokens]
+
+
+def log_likelihood(weights, thresholds, tokens, sparse_from: int | None = None, kv_dtype=None):
+    """Per-token log-likelihood of ``tokens`` under the sparse prompt pass —
+    the evaluation TEAL sparsifies prefill for (the second
+    half of the sequence thresholded by default, log-likelihood tasks and
+    perplexity).  Returns (logp [T-1] fp32 on the device: log p(token[t+1] |
+    tokens[..t]), perplexity = exp(-mean logp))."""
+    tok = torch.as_tensor(tokens, dtype=torch.int64).reshape(-1)
+    r = SparsePrefill(weights, thresholds, kv_dtype=kv_dtype).forward(tokens=tok, sparse_from=sparse_from,
+                                                                     logits="all")
+    lp = torch.log_softmax(r.logits[:-1].double(), dim=-1)
+    tgt = tok[1:].to(lp.device)
+    logp = lp.gather(1, tgt[:, None])[:, 0].float()
+    return logp, float(torch.exp(-logp.double().mean()))

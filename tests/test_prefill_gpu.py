@@ -289,3 +289,22 @@ def test_generate_matches_step_decoding(P):
         dec.step_token()
         want.append(int(dec.token))
     assert got == want
+
+
+def test_log_likelihood_matches_stepwise_logits(P):
+    # the prompt pass with logits="all" gives every position's next-token
+    # distribution: equal to the step engine's logits teacher-forced (dense)
+    from paper_2408_14690_b200 import engine as E
+    W = _llama_toy(seed=10)
+    toks = torch.randint(0, 1024, (24,), generator=torch.Generator().manual_seed(11)).tolist()
+    logp, ppl = P.log_likelihood(W, None, toks, kv_dtype=torch.float32)
+    dec = E.StepDecoder(W, None, kv_dtype=torch.float32)
+    dec.reset()
+    want = []
+    for i, t in enumerate(toks[:-1]):
+        dec.token.fill_(t)
+        dec.step_token()
+        want.append(float(torch.log_softmax(dec.logits.double(), 0)[toks[i + 1]]))
+    want = torch.tensor(want, dtype=torch.float64)
+    assert torch.allclose(logp.cpu().double(), want, atol=1e-4, rtol=0)
+    assert abs(ppl - float(torch.exp(-want.mean()))) / ppl < 1e-4
