@@ -282,21 +282,21 @@ def capture_steps(dec):
     dec.reset()
 
 
-def make_decoder(engine, W, thr, count_kept=False):
+def make_decoder(engine, W, thr, count_kept=False, lm_threshold=None):
     from paper_2408_14690_b200 import decode as D
     from paper_2408_14690_b200 import engine as E
     if engine == "step":
-        return E.StepDecoder(W, thr, count_kept=count_kept)
-    return D.SparseDecoder(W, thr)
+        return E.StepDecoder(W, thr, count_kept=count_kept, lm_threshold=lm_threshold)
+    return D.SparseDecoder(W, thr, lm_threshold=lm_threshold)
 
 
-def decode_tok_s(D, W, thr, steps, warmup, ws, engine="step", gbs_out=None):
+def decode_tok_s(D, W, thr, steps, warmup, ws, engine="step", gbs_out=None, lm_threshold=None):
     """tok/s of `steps` replays; with gbs_out (a dict) and the step engine,
     also the step's algorithmic GB/s (kept channels counted on the device
     during the timed steps), stored under gbs_out["gbs"]."""
     import torch
     count = gbs_out is not None and engine == "step"
-    dec = make_decoder(engine, W, thr, count_kept=count)
+    dec = make_decoder(engine, W, thr, count_kept=count, lm_threshold=lm_threshold)
     capture_steps(dec)
     for _ in range(warmup):
         dec.replay()
@@ -665,8 +665,14 @@ def run_ours(args):
             gtok, _, _ = decode_tok_s(D, W, thr_g, n_sw, 3, ws, args.engine, gbs_out=gl)
             greedy_row = {str(args.sparsity): round(gtok, 2), "hbm_frac": round(gl["gbs"] / peak, 3),
                           "calibration": "32 tokens, alpha 0.05, per-layer block forward error"}
+            # §8(f)#3: the LM head's input thresholded too (t = the 50 % quantile of |N(0,1)|:
+            # the final-norm row has unit RMS); the headline keeps the paper's dense head
+            from paper_2408_14690_b200 import theory as TH
+            lm_tok, _, _ = decode_tok_s(D, W, thr[args.sparsity], n_sw, 3, ws, args.engine,
+                                        lm_threshold=TH.gaussian_threshold(0.5))
+            lm_row = {str(args.sparsity): round(lm_tok, 2), "lm_threshold": "gaussian_threshold(0.5) on the unit-RMS final-norm row"}
         else:
-            greedy_row = None
+            greedy_row = lm_row = None
         if args.engine == "step" and args.contexts:
             sweep_ctx = {}
             for ctx in (int(c) for c in args.contexts.split(",") if c):
@@ -685,6 +691,7 @@ def run_ours(args):
                  "dense_hbm_frac": round(dense_tok * wb / 1e9 / peak, 3),
                  f"decode_tok_s_at_context_{args.sparsity}": dec_rows_ctx,
                  "greedy_decode_tok_s": greedy_row,
+                 "decode_tok_s_thresholded_lm_head": lm_row,
                  "hbm_roofline_frac": frac_rows}
         # sparse prefill (the paper's second-half recipe) on the tcgen05 masked GEMM: TTFT
         sys.path.insert(0, str(ROOT / "scripts"))
